@@ -1,0 +1,299 @@
+// cg.cu — UKAN coefficient generator (CG) MLP: grid-group positional encoding + dense GEMMs.
+//
+// Replaces positional_encoding (layers.py:112-123), _cg_eval (232-243) and the tape
+// backward of its matmul / silu / gather_rows / concat_last (tensor.py:189-197, 228-233,
+// 257-268, 276-285).
+//   inp[r] = [emb[f_r] || PE(g_r)]           PE in fp64 (SURVEY gotcha 3), stored fp32
+//   H      = silu(inp @ W1 + b1)             fp32 GEMM (K = d_femb + d_pe)
+//   Out    = H @ W2 + b2                     fp32 GEMM (K = d_h) -> table [n_u, K*d_out]
+//   backward GEMMs accumulate in fp64 (reductions over n_u / K*d_out).
+// These are CUDA-core tiled GEMMs (first implementation); the tcgen05 3xTF32 path is the
+// planned replacement.
+#include "common.cuh"
+
+namespace ukan {
+
+// ---------------------------------------------------------------------------------------
+// positional encoding + embedding gather
+// ---------------------------------------------------------------------------------------
+constexpr int kMaxPeHalf = 128;
+struct PeFreqs {
+  double f[kMaxPeHalf];
+};
+
+__global__ void cg_input_kernel(const int32_t* __restrict__ key_f,
+                                const int64_t* __restrict__ key_g, const float* __restrict__ emb,
+                                float* __restrict__ inp, int64_t n_u, int d_femb, int d_pe,
+                                PeFreqs fr) {
+  const int W = d_femb + d_pe;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_u * W) return;
+  const int64_t r = t / W;
+  const int c = (int)(t % W);
+  float v;
+  if (c < d_femb) {
+    v = emb[(size_t)key_f[r] * d_femb + c];
+  } else {
+    const int m = (c - d_femb) >> 1;
+    const double ang = (double)key_g[r] * fr.f[m];  // g[..., None] * freqs  (layers.py:119)
+    v = (float)(((c - d_femb) & 1) ? cos(ang) : sin(ang));
+  }
+  inp[t] = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Tiled GEMMs (64x64 CTA tile, 4x4 per thread, BK = 16).
+// ---------------------------------------------------------------------------------------
+constexpr int TM = 64, TN = 64, TK = 16;
+
+// C = act(A[M,K] @ B[K,N] + bias), fp32 accumulate.  pre_out (optional) = pre-activation.
+__global__ void __launch_bounds__(256)
+gemm_nn_kernel(const float* __restrict__ A, const float* __restrict__ Bm,
+               const float* __restrict__ bias, float* __restrict__ C, float* __restrict__ pre,
+               int M, int N, int K, int act) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int t = threadIdx.x; t < TM * TK; t += 256) {
+      const int mm = t / TK, kk = t % TK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? A[(size_t)gm * K + gk] : 0.f;
+    }
+    for (int t = threadIdx.x; t < TK * TN; t += 256) {
+      const int kk = t / TN, nn = t % TN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? Bm[(size_t)gk * N + gn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = As[kk][ty * 4 + q];
+        b[q] = Bs[kk][tx * 4 + q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int gm = m0 + ty * 4 + p;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gn = n0 + tx * 4 + q;
+      if (gn >= N) continue;
+      float v = acc[p][q] + (bias ? bias[gn] : 0.f);
+      if (pre) pre[(size_t)gm * N + gn] = v;
+      if (act == 1) v = (float)silu_d((double)v);
+      C[(size_t)gm * N + gn] = v;
+    }
+  }
+}
+
+// C[M,N] = A[M,K] @ B[N,K]^T, fp64 accumulate.
+__global__ void __launch_bounds__(256)
+gemm_nt_kernel(const float* __restrict__ A, const float* __restrict__ Bm, float* __restrict__ C,
+               int M, int N, int K) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int t = threadIdx.x; t < TM * TK; t += 256) {
+      const int mm = t / TK, kk = t % TK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? A[(size_t)gm * K + gk] : 0.f;
+    }
+    for (int t = threadIdx.x; t < TN * TK; t += 256) {
+      const int nn = t / TK, kk = t % TK;
+      const int gn = n0 + nn, gk = k0 + kk;
+      Bs[kk][nn] = (gn < N && gk < K) ? Bm[(size_t)gn * K + gk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = (double)As[kk][ty * 4 + q];
+        b[q] = (double)Bs[kk][tx * 4 + q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int gm = m0 + ty * 4 + p;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gn = n0 + tx * 4 + q;
+      if (gn < N) C[(size_t)gm * N + gn] = (float)acc[p][q];
+    }
+  }
+}
+
+// C[M,N] = A[K,M]^T @ B[K,N], fp64 accumulate over the (long) K = n_u dimension.
+__global__ void __launch_bounds__(256)
+gemm_tn_kernel(const float* __restrict__ A, const float* __restrict__ Bm, float* __restrict__ C,
+               int M, int N, int K) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int t = threadIdx.x; t < TK * TM; t += 256) {
+      const int kk = t / TM, mm = t % TM;
+      const int gk = k0 + kk, gm = m0 + mm;
+      As[kk][mm] = (gk < K && gm < M) ? A[(size_t)gk * M + gm] : 0.f;
+    }
+    for (int t = threadIdx.x; t < TK * TN; t += 256) {
+      const int kk = t / TN, nn = t % TN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? Bm[(size_t)gk * N + gn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = (double)As[kk][ty * 4 + q];
+        b[q] = (double)Bs[kk][tx * 4 + q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int gm = m0 + ty * 4 + p;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gn = n0 + tx * 4 + q;
+      if (gn < N) C[(size_t)gm * N + gn] = (float)acc[p][q];
+    }
+  }
+}
+
+// colsum[n] = sum_k B[k, n] in fp64 (bias gradients), fixed order.
+__global__ void colsum_kernel(const float* __restrict__ Bm, float* __restrict__ out, int K, int N) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int k = 0; k < K; ++k) s += (double)Bm[(size_t)k * N + n];
+  out[n] = (float)s;
+}
+
+__global__ void silu_bwd_kernel(const float* __restrict__ pre, const float* __restrict__ dH,
+                                float* __restrict__ dpre, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  dpre[t] = (float)((double)dH[t] * dsilu_d((double)pre[t]));
+}
+
+// d_emb[f, c] = sum_{r in seg(f)} dinp[r, c], c < d_femb, fp64, key order.
+__global__ void emb_bwd_kernel(const int32_t* __restrict__ seg_start,
+                               const float* __restrict__ dinp, float* __restrict__ d_emb,
+                               int d_in, int d_femb, int d_cg_in) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)d_in * d_femb) return;
+  const int f = (int)(t / d_femb), c = (int)(t % d_femb);
+  double s = 0.0;
+  for (int r = seg_start[f]; r < seg_start[f + 1]; ++r) s += (double)dinp[(size_t)r * d_cg_in + c];
+  d_emb[t] = (float)s;
+}
+
+}  // namespace ukan
+
+using namespace ukan;
+
+extern "C" int ukan_ukan_cg_input(const int32_t* key_f, const int64_t* key_g, const float* emb,
+                                  float* inp, int64_t n_u, int64_t d_femb, int64_t d_pe,
+                                  void* stream) {
+  if (d_pe % 2 != 0 || d_pe / 2 > kMaxPeHalf || d_femb < 0 || n_u < 0) return UKAN_E_ARG;
+  if (n_u == 0) return UKAN_OK;
+  PeFreqs fr;
+  for (int m = 0; m < d_pe / 2; ++m)  // freqs = 10000.0 ** (-2.0 * arange(half) / d_pe)
+    fr.f[m] = pow(10000.0, (-2.0 * (double)m) / (double)d_pe);
+  const int64_t n = n_u * (d_femb + d_pe);
+  cg_input_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      key_f, key_g, emb, inp, n_u, (int)d_femb, (int)d_pe, fr);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_gemm_bias_act(const float* A, const float* Bm, const float* bias, float* C,
+                                  float* pre_out, int64_t M, int64_t N, int64_t K, int act,
+                                  void* stream) {
+  if (M < 0 || N < 1 || K < 1 || M > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
+  if (M == 0) return UKAN_OK;
+  dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
+  gemm_nn_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(A, Bm, bias, C, pre_out, (int)M, (int)N, (int)K, act);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_gemm_nt(const float* A, const float* Bm, float* C, int64_t M, int64_t N,
+                            int64_t K, void* stream) {
+  if (M < 0 || N < 1 || K < 1 || M > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
+  if (M == 0) return UKAN_OK;
+  dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
+  gemm_nt_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(A, Bm, C, (int)M, (int)N, (int)K);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_gemm_tn(const float* A, const float* Bm, float* C, float* colsum_B,
+                            int64_t M, int64_t N, int64_t K, void* stream) {
+  if (M < 1 || N < 1 || K < 0 || K > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
+  gemm_tn_kernel<<<g, 256, 0, st>>>(A, Bm, C, (int)M, (int)N, (int)K);
+  UKAN_LAUNCH_CHECK();
+  if (colsum_B) {
+    colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(Bm, colsum_B, (int)K, (int)N);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
+
+extern "C" int ukan_silu_backward(const float* pre, const float* dH, float* dpre, int64_t n,
+                                  void* stream) {
+  if (n < 0 || !pre || !dH || !dpre) return UKAN_E_ARG;
+  if (n == 0) return UKAN_OK;
+  silu_bwd_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(pre, dH, dpre, n);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_ukan_emb_backward(const int32_t* seg_start, const float* dinp, float* d_emb,
+                                      int64_t d_in, int64_t d_femb, int64_t d_cg_in,
+                                      void* stream) {
+  if (d_in < 1 || d_femb < 0 || d_cg_in < d_femb || !seg_start || !d_emb) return UKAN_E_ARG;
+  const int64_t n = d_in * d_femb;
+  if (n == 0) return UKAN_OK;
+  emb_bwd_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      seg_start, dinp, d_emb, (int)d_in, (int)d_femb, (int)d_cg_in);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}

@@ -1,0 +1,679 @@
+// spline.cu — matrix-form B-spline layer kernels shared by KAN and UKAN.
+//
+// Reference path (float64 NumPy, /root/reference/pkg/src/ukan/layers.py):
+//   KAN  kan_forward 304-318 = _kan_locate 294-301 -> span_gather 57-75 -> basis_features 40-54
+//        -> edge_combine 78-105 (+ base branch 316-317)
+//   UKAN ukan_forward 254-291: same span_gather/basis_features/edge_combine over the
+//        generator's coefficient table, rows/cols from 284-287.
+//   backward = the bwd closures 44-46, 67-70, 84-88 (+ clamp tensor.py:327-338 for KAN).
+//
+// Both layers evaluate  y[b,o] = sum_i scale[i,o] * sum_j w_j(u_bi) * T[row_bi + j, o]
+// over a row-major table T[rows, d_out]:
+//   KAN : T = coeffs viewed as [d_in*(G+k), d_out], row_bi = i*(G+k) + cell_bi
+//   UKAN: T = CG output viewed as [n_u*K, d_out] (slot-major), row_bi = base_row[b,i]; with
+//         feature-major key order the K rows of a window are consecutive (see ukan_b200.h).
+// Each feature i owns a contiguous row segment [row0_i, row0_i + R_i) of T.
+#include "common.cuh"
+
+namespace ukan {
+
+KanGrid make_kan_grid(double g_min, double g_max, int64_t G) {
+  KanGrid g;
+  g.g_min = g_min;
+  g.hi = nextafter(g_max, g_min);
+  g.dg = (g_max - g_min) / (double)G;
+  g.inv_dg = 1.0 / g.dg;
+  g.gmin_dg = g_min / g.dg;
+  g.G = (int)G;
+  return g;
+}
+
+// How a layer maps (b, i) to a table row and in-cell position.
+struct RowMap {
+  // KAN
+  KanGrid grid;
+  int R;  // G + k
+  // UKAN
+  double inv_dg;
+  const int32_t* base_row;   // [B, d_in]
+  const int32_t* seg_start;  // [d_in + 1]
+  int K;
+};
+
+template <bool UKAN>
+__device__ __forceinline__ bool locate_row(const RowMap& rm, float xv, int64_t b, int i,
+                                           int d_in, int& row, double& u, bool& mask) {
+  if constexpr (UKAN) {
+    int64_t gid;
+    ukan_locate(xv, rm.inv_dg, gid, u);
+    row = rm.base_row[(size_t)b * d_in + i];
+    mask = true;
+    return true;
+  } else {
+    int cell;
+    const bool ok = kan_locate(xv, rm.grid, cell, u, mask);
+    row = i * rm.R + cell;
+    return ok;
+  }
+}
+
+template <bool UKAN>
+__device__ __forceinline__ void feature_rows(const RowMap& rm, int i, int& row0, int& nrows) {
+  if constexpr (UKAN) {
+    const int s0 = rm.seg_start[i], s1 = rm.seg_start[i + 1];
+    row0 = s0 * rm.K;
+    nrows = (s1 - s0) * rm.K;
+  } else {
+    row0 = i * rm.R;
+    nrows = rm.R;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Forward.
+// CTA tile = Bt samples x Ot outputs; blockDim = (TO, TS); each thread owns S samples x VEC
+// consecutive outputs in registers and sweeps all d_in features.  Per stage of FC features
+// the CTA computes (fp64 locate, fp64 basis -> fp32 weights) once for its Bt x FC
+// (sample, feature) pairs into shared memory; then every thread gathers its K table rows
+// with vector loads through the read-only path (the per-feature slab stays L1-resident while
+// the CTA works on it) and accumulates, in edge_combine's order,
+//   y[b,o] += scale[i,o] * (sum_j w_j * T[row + j, o])                      (fp32)
+// ---------------------------------------------------------------------------------------
+constexpr int kFwdFC = 8;
+constexpr int kFwdS = 4;
+
+template <int K, int VEC, bool UKAN>
+__global__ void __launch_bounds__(256, 2)
+spline_fwd_kernel(const float* __restrict__ x, const float* __restrict__ T,
+                  const float* __restrict__ scale, const float* __restrict__ bw,
+                  float* __restrict__ y, int B, int d_in, int d_out, RowMap rm, Basis<K> bas,
+                  int32_t* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int TO = blockDim.x, TS = blockDim.y;
+  const int Bt = TS * kFwdS;
+  int* row_s = reinterpret_cast<int*>(smem_raw);                 // [FC][Bt]
+  float* w_s = reinterpret_cast<float*>(row_s + kFwdFC * Bt);    // [FC][Bt][K]
+  float* sl_s = w_s + kFwdFC * Bt * K;                           // [FC][Bt] silu(x)
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TO + tx, nthr = TO * TS;
+  const int b0 = blockIdx.x * Bt;
+  const int o = blockIdx.y * (TO * VEC) + tx * VEC;
+  const bool o_ok = o < d_out;
+  const bool has_base = bw != nullptr;
+
+  float acc[kFwdS][VEC];
+#pragma unroll
+  for (int r = 0; r < kFwdS; ++r)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[r][v] = 0.f;
+
+  for (int f0 = 0; f0 < d_in; f0 += kFwdFC) {
+    __syncthreads();
+    for (int p = tid; p < kFwdFC * Bt; p += nthr) {
+      const int s = p / kFwdFC, f = p % kFwdFC;
+      const int b = b0 + s, i = f0 + f;
+      int row = -1;
+      if (b < B && i < d_in) {
+        const float xv = x[(size_t)b * d_in + i];
+        double u;
+        bool mask;
+        if (!locate_row<UKAN>(rm, xv, b, i, d_in, row, u, mask)) {
+          if (err) atomicExch(err, 1);
+          row = UKAN ? row : i * rm.R;
+          u = 0.0;
+        }
+        double w[K];
+        basis_weights<K>(bas, u, w);
+#pragma unroll
+        for (int j = 0; j < K; ++j) w_s[(f * Bt + s) * K + j] = (float)w[j];
+        if (has_base) sl_s[f * Bt + s] = (float)silu_d((double)xv);
+      }
+      row_s[f * Bt + s] = row;
+    }
+    __syncthreads();
+    if (!o_ok) continue;
+    const int nf = min(kFwdFC, d_in - f0);
+    for (int f = 0; f < nf; ++f) {
+      const int i = f0 + f;
+      float sc[VEC], bv[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        sc[v] = __ldg(scale + (size_t)i * d_out + o + v);
+        bv[v] = has_base ? __ldg(bw + (size_t)i * d_out + o + v) : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < kFwdS; ++r) {
+        const int s = ty + TS * r;
+        const int row = row_s[f * Bt + s];
+        if (row < 0) continue;
+        const float* rp = T + (size_t)row * d_out + o;
+        float tmp[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) tmp[v] = 0.f;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float wj = w_s[(f * Bt + s) * K + j];
+          const float* q = rp + (size_t)j * d_out;
+          if constexpr (VEC == 4) {
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(q));
+            tmp[0] = fmaf(wj, cv.x, tmp[0]);
+            tmp[1] = fmaf(wj, cv.y, tmp[1]);
+            tmp[2] = fmaf(wj, cv.z, tmp[2]);
+            tmp[3] = fmaf(wj, cv.w, tmp[3]);
+          } else if constexpr (VEC == 2) {
+            const float2 cv = __ldg(reinterpret_cast<const float2*>(q));
+            tmp[0] = fmaf(wj, cv.x, tmp[0]);
+            tmp[1] = fmaf(wj, cv.y, tmp[1]);
+          } else {
+            tmp[0] = fmaf(wj, __ldg(q), tmp[0]);
+          }
+        }
+        const float sl = has_base ? sl_s[f * Bt + s] : 0.f;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          acc[r][v] = fmaf(sc[v], tmp[v], acc[r][v]);
+          if (has_base) acc[r][v] = fmaf(sl, bv[v], acc[r][v]);
+        }
+      }
+    }
+  }
+  if (!o_ok) return;
+#pragma unroll
+  for (int r = 0; r < kFwdS; ++r) {
+    const int b = b0 + ty + TS * r;
+    if (b >= B) continue;
+    float* yr = y + (size_t)b * d_out + o;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) yr[v] = acc[r][v];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Warp-level bitonic sort of 32*P int keys held P per lane (element e = lane*P + q).
+// ---------------------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void warp_bitonic_sort(int (&a)[P], int lane) {
+  constexpr int N = 32 * P;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= P) {
+        const int lm = j / P;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const int e = lane * P + q;
+          const int other = __shfl_xor_sync(0xffffffffu, a[q], lm);
+          const bool lower = (e & j) == 0;
+          const bool asc = (e & k) == 0;
+          a[q] = (lower == asc) ? min(a[q], other) : max(a[q], other);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          if ((q & j) == 0) {
+            const int q2 = q | j;
+            const int e = lane * P + q;
+            const bool asc = (e & k) == 0;
+            const int lo = min(a[q], a[q2]), hi = max(a[q], a[q2]);
+            a[q] = asc ? lo : hi;
+            a[q2] = asc ? hi : lo;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Backward, table side:  A[row, o] = sum_{(b,j): row_bi + j = row} w_j(b,i) * g[b,o]
+//   dT = scale * A,  dscale = sum_rows T * A,  dbw = sum_b silu(x) * g   (KAN base branch).
+// One warp per feature i, lanes over OV consecutive outputs; a CTA holds FT features and
+// sweeps the whole batch in chunks of BC samples, so each (row, o) is owned by exactly one
+// thread: no atomics, fixed summation order -> deterministic.  Per chunk the warp sorts its
+// BC samples by (row, sample) with a register bitonic network and streams them in row order
+// through a sliding window of K fp64 register accumulators; a row leaving the window is
+// added into the fp64 accumulator A (shared memory when the feature's segment fits, a
+// global fp64 workspace otherwise).  Products are fp64 basis weights x exactly-upcast fp32
+// g, accumulated in fp64.
+// ---------------------------------------------------------------------------------------
+constexpr int kBwdBC = 128;
+
+template <int K, int OV, bool A_SMEM, bool UKAN>
+__global__ void __launch_bounds__(256, 2)
+spline_bwd_table_kernel(const float* __restrict__ x, const float* __restrict__ T,
+                        const float* __restrict__ scale, const float* __restrict__ gy,
+                        float* __restrict__ dT, float* __restrict__ dscale,
+                        float* __restrict__ dbw, double* __restrict__ A_glob, int B, int d_in,
+                        int d_out, int R_smem, RowMap rm, Basis<K> bas) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int OT = 32 * OV;
+  constexpr int P = kBwdBC / 32;
+  const int FT = blockDim.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int i = blockIdx.x * FT + warp;
+  const int o0 = blockIdx.y * OT;
+  const bool has_base = dbw != nullptr;
+
+  unsigned char* p = smem_raw;
+  double* A_s = reinterpret_cast<double*>(p);  // [FT][R_smem][OT]
+  if (A_SMEM) p += sizeof(double) * (size_t)FT * R_smem * OT;
+  double* w_s = reinterpret_cast<double*>(p);  // [FT][BC][K]
+  p += sizeof(double) * FT * kBwdBC * K;
+  double* sl_s = reinterpret_cast<double*>(p);  // [FT][BC]
+  p += sizeof(double) * FT * kBwdBC;
+  float* g_s = reinterpret_cast<float*>(p);  // [BC][OT]
+  p += sizeof(float) * kBwdBC * OT;
+  int* ent_s = reinterpret_cast<int*>(p);  // [FT][BC]  (local_row << 8 | s)
+
+  const bool active = i < d_in;
+  int row0 = 0, nrows = 0;
+  if (active) feature_rows<UKAN>(rm, i, row0, nrows);
+  double* A = A_SMEM ? A_s + (size_t)warp * R_smem * OT : A_glob + (size_t)row0 * d_out;
+  const int a_stride = A_SMEM ? OT : d_out;
+  const int a_col = A_SMEM ? lane * OV : o0 + lane * OV;
+  bool ovalid[OV];
+#pragma unroll
+  for (int v = 0; v < OV; ++v) ovalid[v] = (o0 + lane * OV + v) < d_out;
+
+  if (active) {
+    for (int r = 0; r < nrows; ++r)
+#pragma unroll
+      for (int v = 0; v < OV; ++v)
+        if (A_SMEM || ovalid[v]) A[(size_t)r * a_stride + a_col + v] = 0.0;
+  }
+  double bacc[OV];
+#pragma unroll
+  for (int v = 0; v < OV; ++v) bacc[v] = 0.0;
+
+  int* ent = ent_s + warp * kBwdBC;
+  double* wsw = w_s + (size_t)warp * kBwdBC * K;
+  double* slw = sl_s + warp * kBwdBC;
+
+  for (int b0 = 0; b0 < B; b0 += kBwdBC) {
+    const int nb = min(kBwdBC, B - b0);
+    __syncthreads();  // previous chunk fully consumed
+    for (int t = threadIdx.x; t < kBwdBC * OT; t += blockDim.x) {
+      const int s = t / OT, oc = t % OT;
+      float gv = 0.f;
+      if (s < nb && o0 + oc < d_out) gv = gy[(size_t)(b0 + s) * d_out + o0 + oc];
+      g_s[t] = gv;
+    }
+    if (active) {
+      int keys[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const int s = lane * P + q;
+        int key = INT_MAX;
+        if (s < nb) {
+          const float xv = x[(size_t)(b0 + s) * d_in + i];
+          int row;
+          double u;
+          bool mask;
+          locate_row<UKAN>(rm, xv, b0 + s, i, d_in, row, u, mask);
+          double w[K];
+          basis_weights<K>(bas, u, w);
+#pragma unroll
+          for (int j = 0; j < K; ++j) wsw[s * K + j] = w[j];
+          if (has_base) slw[s] = silu_d((double)xv);
+          key = ((row - row0) << 8) | s;
+        }
+        keys[q] = key;
+      }
+      warp_bitonic_sort<P>(keys, lane);
+#pragma unroll
+      for (int q = 0; q < P; ++q) ent[lane * P + q] = keys[q];
+    }
+    __syncthreads();  // g_s staged, entries sorted
+    if (!active) continue;
+
+    double acc[K][OV];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+      for (int v = 0; v < OV; ++v) acc[j][v] = 0.0;
+    int cur = -1;
+    for (int e = 0; e < nb; ++e) {
+      const int pk = ent[e];
+      const int c = pk >> 8, s = pk & 255;
+      if (c != cur) {
+        if (cur >= 0) {
+          const int d = c - cur;
+#pragma unroll
+          for (int t = 0; t < K; ++t) {
+            if (t < d) {
+              if (cur + t < nrows) {
+#pragma unroll
+                for (int v = 0; v < OV; ++v)
+                  if (A_SMEM || ovalid[v]) A[(size_t)(cur + t) * a_stride + a_col + v] += acc[0][v];
+              }
+#pragma unroll
+              for (int jj = 0; jj < K - 1; ++jj)
+#pragma unroll
+                for (int v = 0; v < OV; ++v) acc[jj][v] = acc[jj + 1][v];
+#pragma unroll
+              for (int v = 0; v < OV; ++v) acc[K - 1][v] = 0.0;
+            }
+          }
+        }
+        cur = c;
+      }
+      double gv[OV];
+#pragma unroll
+      for (int v = 0; v < OV; ++v) gv[v] = (double)g_s[s * OT + lane * OV + v];
+      const double* we = wsw + s * K;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const double wj = we[j];
+#pragma unroll
+        for (int v = 0; v < OV; ++v) acc[j][v] = fma(wj, gv[v], acc[j][v]);
+      }
+      if (has_base) {
+        const double sl = slw[s];
+#pragma unroll
+        for (int v = 0; v < OV; ++v) bacc[v] = fma(sl, gv[v], bacc[v]);
+      }
+    }
+    if (cur >= 0) {
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+        if (cur + t < nrows)
+#pragma unroll
+          for (int v = 0; v < OV; ++v)
+            if (A_SMEM || ovalid[v]) A[(size_t)(cur + t) * a_stride + a_col + v] += acc[t][v];
+    }
+  }
+  if (!active) return;
+  __syncwarp();
+#pragma unroll
+  for (int v = 0; v < OV; ++v) {
+    const int o = o0 + lane * OV + v;
+    if (!ovalid[v]) continue;
+    const double sc = (double)scale[(size_t)i * d_out + o];
+    double ds = 0.0;
+    for (int r = 0; r < nrows; ++r) {
+      const double a = A[(size_t)r * a_stride + a_col + v];
+      const size_t ti = (size_t)(row0 + r) * d_out + o;
+      dT[ti] = (float)(sc * a);
+      ds = fma((double)T[ti], a, ds);
+    }
+    dscale[(size_t)i * d_out + o] = (float)ds;
+    if (has_base) dbw[(size_t)i * d_out + o] = (float)bacc[v];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Backward, input side:
+//   dx[b,i] = mask * inv_dg * sum_j w'_j * sum_o g[b,o]*scale[i,o]*T[row+j,o]
+//             (+ dsilu(x) * sum_o g[b,o]*bw[i,o])                               (KAN)
+// (UKAN: u = x*inv_dg - g_id, so du/dx = inv_dg and there is no clamp mask.)
+// One warp per (b, i), lanes over d_out, fp64 products/accumulators, shuffle reduction.
+// ---------------------------------------------------------------------------------------
+template <int K, bool UKAN>
+__global__ void __launch_bounds__(256)
+spline_dx_kernel(const float* __restrict__ x, const float* __restrict__ T,
+                 const float* __restrict__ scale, const float* __restrict__ bw,
+                 const float* __restrict__ gy, float* __restrict__ dx, int B, int d_in,
+                 int d_out, RowMap rm, Basis<K> bas) {
+  const int lane = threadIdx.x % 32;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (pair >= (int64_t)B * d_in) return;
+  const int b = (int)(pair / d_in), i = (int)(pair % d_in);
+  const float xv = x[(size_t)b * d_in + i];
+  int row;
+  double u;
+  bool mask;
+  locate_row<UKAN>(rm, xv, b, i, d_in, row, u, mask);
+  double wp[K];
+  basis_dweights<K>(bas, u, wp);
+  double S[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) S[j] = 0.0;
+  double sb = 0.0;
+  const float* Ti = T + (size_t)row * d_out;
+  const float* gr = gy + (size_t)b * d_out;
+  for (int o = lane; o < d_out; o += 32) {
+    const double g = (double)gr[o];
+    const double gs = g * (double)scale[(size_t)i * d_out + o];
+#pragma unroll
+    for (int j = 0; j < K; ++j) S[j] = fma(gs, (double)Ti[(size_t)j * d_out + o], S[j]);
+    if (bw) sb = fma(g, (double)bw[(size_t)i * d_out + o], sb);
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) t = fma(S[j], wp[j], t);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    t += __shfl_xor_sync(0xffffffffu, t, off);
+    sb += __shfl_xor_sync(0xffffffffu, sb, off);
+  }
+  if (lane == 0) {
+    const double inv = UKAN ? rm.inv_dg : rm.grid.inv_dg;
+    double d = mask ? t * inv : 0.0;
+    if (bw) d += dsilu_d((double)xv) * sb;
+    dx[(size_t)b * d_in + i] = (float)d;
+  }
+}
+
+__global__ void kan_locate_kernel(const float* __restrict__ x, int32_t* __restrict__ cell,
+                                  double* __restrict__ u, int64_t n, KanGrid grid) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int c;
+  double uu;
+  bool mask;
+  kan_locate(x[t], grid, c, uu, mask);
+  cell[t] = c;
+  u[t] = uu;
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+constexpr size_t kSmemCap = 220 * 1024;
+constexpr int kBwdOV = 2;
+
+static size_t bwd_smem_bytes(int K, int FT, int OT, int R, bool a_smem) {
+  size_t s = 0;
+  if (a_smem) s += sizeof(double) * (size_t)FT * R * OT;
+  s += sizeof(double) * FT * kBwdBC * K;
+  s += sizeof(double) * FT * kBwdBC;
+  s += sizeof(float) * kBwdBC * OT;
+  s += sizeof(int) * FT * kBwdBC;
+  return s;
+}
+
+static bool bwd_fits_smem(int K, int R) { return bwd_smem_bytes(K, 1, 32 * kBwdOV, R, true) <= kSmemCap; }
+
+template <int K, bool UKAN>
+static int launch_fwd(const float* x, const float* T, const float* scale, const float* bw,
+                      float* y, int B, int d_in, int d_out, const RowMap& rm, int32_t* err,
+                      cudaStream_t st) {
+  const Basis<K> bas = make_basis<K>(K - 1);
+  const int VEC = (d_out % 4 == 0) ? 4 : (d_out % 2 == 0 ? 2 : 1);
+  int TO = (d_out + VEC - 1) / VEC;
+  if (TO > 32) TO = 32;
+  int TS = 256 / TO;
+  if (TS > 64) TS = 64;
+  const int Bt = TS * kFwdS;
+  dim3 block(TO, TS);
+  dim3 gridd((B + Bt - 1) / Bt, (d_out + TO * VEC - 1) / (TO * VEC));
+  const size_t smem = (size_t)kFwdFC * Bt * (sizeof(int) + sizeof(float) * (K + 1));
+  if (VEC == 4)
+    spline_fwd_kernel<K, 4, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
+  else if (VEC == 2)
+    spline_fwd_kernel<K, 2, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
+  else
+    spline_fwd_kernel<K, 1, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+template <int K, bool UKAN>
+static int launch_bwd(const float* x, const float* T, const float* scale, const float* bw,
+                      const float* gy, float* dx, float* dT, float* dscale, float* dbw,
+                      double* A_glob, int B, int d_in, int d_out, int R_max, const RowMap& rm,
+                      cudaStream_t st) {
+  const Basis<K> bas = make_basis<K>(K - 1);
+  constexpr int OV = kBwdOV;
+  constexpr int OT = 32 * OV;
+  int FT = 8;
+  bool a_smem = true;
+  while (FT > 1 && bwd_smem_bytes(K, FT, OT, R_max, true) > kSmemCap) FT >>= 1;
+  if (bwd_smem_bytes(K, FT, OT, R_max, true) > kSmemCap) {
+    a_smem = false;
+    FT = 8;
+    if (A_glob == nullptr) return UKAN_E_WORKSPACE;
+  }
+  const size_t smem = bwd_smem_bytes(K, FT, OT, R_max, a_smem);
+  dim3 gridd((d_in + FT - 1) / FT, (d_out + OT - 1) / OT);
+  if (a_smem) {
+    auto kern = spline_bwd_table_kernel<K, OV, true, UKAN>;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<gridd, FT * 32, smem, st>>>(x, T, scale, gy, dT, dscale, dbw, nullptr, B, d_in, d_out, R_max, rm, bas);
+  } else {
+    auto kern = spline_bwd_table_kernel<K, OV, false, UKAN>;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<gridd, FT * 32, smem, st>>>(x, T, scale, gy, dT, dscale, dbw, A_glob, B, d_in, d_out, 0, rm, bas);
+  }
+  UKAN_LAUNCH_CHECK();
+  if (dx) {
+    const int64_t pairs = (int64_t)B * d_in;
+    if (pairs > 0) {
+      const int wpb = 8;
+      spline_dx_kernel<K, UKAN><<<(unsigned)((pairs + wpb - 1) / wpb), wpb * 32, 0, st>>>(
+          x, T, scale, bw, gy, dx, B, d_in, d_out, rm, bas);
+      UKAN_LAUNCH_CHECK();
+    }
+  }
+  return UKAN_OK;
+}
+
+static int check_kan_args(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
+                          double g_min, double g_max) {
+  if (k < 0 || k > UKAN_MAX_DEGREE) return UKAN_E_DEGREE;
+  if (!(g_min < g_max) || G < 1) return UKAN_E_GRID;
+  if (B < 0 || d_in < 1 || d_out < 1) return UKAN_E_ARG;
+  if (B > INT32_MAX || d_in * (G + k) >= ((int64_t)1 << 31) || (G + k) >= (1 << 23)) return UKAN_E_ARG;
+  return UKAN_OK;
+}
+
+}  // namespace ukan
+
+using namespace ukan;
+
+extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float* scale,
+                                const float* base_weight, float* y, int64_t B, int64_t d_in,
+                                int64_t d_out, int64_t G, int k, double g_min, double g_max,
+                                int32_t* err_flag, void* stream) {
+  int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
+  if (rc) return rc;
+  if (!x || !coeffs || !scale || !y) return UKAN_E_ARG;
+  if (B == 0) return UKAN_OK;
+  RowMap rm{};
+  rm.grid = make_kan_grid(g_min, g_max, G);
+  rm.R = (int)(G + k);
+  cudaStream_t st = (cudaStream_t)stream;
+  UKAN_DISPATCH_K(k, return launch_fwd<K, false>(x, coeffs, scale, base_weight, y, (int)B, (int)d_in, (int)d_out, rm, err_flag, st););
+  return UKAN_OK;
+}
+
+extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
+                                                    int64_t G, int k) {
+  (void)B;
+  if (k < 0 || k > UKAN_MAX_DEGREE || G < 1) return 0;
+  if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
+  return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
+}
+
+extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,
+                                   const float* base_weight, const float* gy, float* dx,
+                                   float* dcoeffs, float* dscale, float* dbase_weight,
+                                   int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
+                                   double g_min, double g_max, void* workspace,
+                                   int64_t workspace_bytes, void* stream) {
+  int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
+  if (rc) return rc;
+  if (!x || !coeffs || !scale || !gy || !dcoeffs || !dscale) return UKAN_E_ARG;
+  if ((base_weight == nullptr) != (dbase_weight == nullptr)) return UKAN_E_ARG;
+  const int64_t need = ukan_kan_backward_workspace_size(B, d_in, d_out, G, k);
+  if (need > 0 && (workspace == nullptr || workspace_bytes < need)) return UKAN_E_WORKSPACE;
+  RowMap rm{};
+  rm.grid = make_kan_grid(g_min, g_max, G);
+  rm.R = (int)(G + k);
+  cudaStream_t st = (cudaStream_t)stream;
+  UKAN_DISPATCH_K(k, return launch_bwd<K, false>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, (double*)workspace, (int)B, (int)d_in, (int)d_out, rm.R, rm, st););
+  return UKAN_OK;
+}
+
+extern "C" int ukan_kan_backward(const float* x, const float* coeffs, const float* scale,
+                                 const float* base_weight, const float* gy, float* dx,
+                                 float* dcoeffs, float* dscale, float* dbase_weight, int64_t B,
+                                 int64_t d_in, int64_t d_out, int64_t G, int k, double g_min,
+                                 double g_max, void* stream) {
+  return ukan_kan_backward_ws(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale,
+                              dbase_weight, B, d_in, d_out, G, k, g_min, g_max, nullptr, 0,
+                              stream);
+}
+
+extern "C" int ukan_kan_locate(const float* x, int32_t* cell, double* u, int64_t B,
+                               int64_t d_in, int64_t G, double g_min, double g_max,
+                               void* stream) {
+  if (!(g_min < g_max) || G < 1) return UKAN_E_GRID;
+  if (!x || !cell || !u || B < 0 || d_in < 1) return UKAN_E_ARG;
+  const int64_t n = B * d_in;
+  if (n == 0) return UKAN_OK;
+  const KanGrid grid = make_kan_grid(g_min, g_max, G);
+  kan_locate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, cell, u, n, grid);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_ukan_forward(const float* x, const int32_t* base_row, const float* table,
+                                 const float* scale, float* y, int64_t B, int64_t d_in,
+                                 int64_t d_out, int k, double delta_g, void* stream) {
+  if (k < 0 || k > UKAN_MAX_DEGREE) return UKAN_E_DEGREE;
+  if (!(delta_g > 0)) return UKAN_E_GRID;
+  if (!x || !base_row || !table || !scale || !y || B < 0 || d_in < 1 || d_out < 1 || B > INT32_MAX)
+    return UKAN_E_ARG;
+  if (B == 0) return UKAN_OK;
+  RowMap rm{};
+  rm.inv_dg = 1.0 / delta_g;  // layers.py:261
+  rm.base_row = base_row;
+  rm.K = k + 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  UKAN_DISPATCH_K(k, return launch_fwd<K, true>(x, table, scale, nullptr, y, (int)B, (int)d_in, (int)d_out, rm, nullptr, st););
+  return UKAN_OK;
+}
+
+extern "C" int64_t ukan_ukan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
+                                                     int64_t n_u, int k) {
+  (void)B;
+  (void)d_in;
+  return (int64_t)sizeof(double) * n_u * (k + 1) * d_out;
+}
+
+extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
+                                  const int32_t* seg_start, const float* table,
+                                  const float* scale, const float* gy, float* dx, float* dtable,
+                                  float* dscale, int64_t B, int64_t d_in, int64_t d_out,
+                                  int64_t n_u, int k, double delta_g, void* workspace,
+                                  int64_t workspace_bytes, void* stream) {
+  if (k < 0 || k > UKAN_MAX_DEGREE) return UKAN_E_DEGREE;
+  if (!(delta_g > 0)) return UKAN_E_GRID;
+  if (!x || !base_row || !seg_start || !table || !scale || !gy || !dtable || !dscale || B < 0 ||
+      d_in < 1 || d_out < 1 || B > INT32_MAX || n_u * (k + 1) >= ((int64_t)1 << 31))
+    return UKAN_E_ARG;
+  const int64_t need = ukan_ukan_backward_workspace_size(B, d_in, d_out, n_u, k);
+  if (workspace == nullptr || workspace_bytes < need) return UKAN_E_WORKSPACE;
+  RowMap rm{};
+  rm.inv_dg = 1.0 / delta_g;
+  rm.base_row = base_row;
+  rm.seg_start = seg_start;
+  rm.K = k + 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  // the fp64 accumulator lives in the global workspace (feature segments are data dependent)
+  UKAN_DISPATCH_K(k, return launch_bwd<K, true>(x, table, scale, nullptr, gy, dx, dtable, dscale, nullptr, (double*)workspace, (int)B, (int)d_in, (int)d_out, 1 << 30, rm, st););
+  return UKAN_OK;
+}

@@ -1,0 +1,243 @@
+"""Data-parallel training step for spline stacks (reference: train.step, train.py:142-150).
+
+``SplineTrainer.step`` = forward through every layer (fused kernels), loss (fp64,
+normalised by the GLOBAL batch), backward through every layer writing parameter gradients
+straight into one flat fp32 gradient buffer, one bucketed NCCL all-reduce(sum) of that buffer
+(per layer, issued as soon as the layer's backward is enqueued so it overlaps the backward of
+the layers below), and one fused Adam (coupled L2) / SGD kernel over the flat parameter
+buffer.  The loss is all-reduced too and guards the optimizer: a non-finite global loss skips
+the update on the device and raises ``DivergedError`` when the host reads it — the
+reference's check-before-update semantics (train.py:143-144) without a mid-step sync.
+
+Everything runs through the C ABI; no autograd tape is recorded on this path (the autograd
+``ops`` are the drop-in layer API; both call the same kernels).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr
+from .errors import ConfigError, DivergedError
+from .layers import KanLayer, Model, UkanLayer
+from . import ops
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous batch shard [lo, hi) of rank (remainder rows go to the first ranks)."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class GradSync:
+    """All-reduce(sum) helper over a torch.distributed group (NCCL on GPUs, gloo in CPU tests).
+    World size 1 (or no initialised group) is a no-op."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.enabled = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        self.world = dist.get_world_size(group) if self.enabled else 1
+        self.rank = dist.get_rank(group) if self.enabled else 0
+        self._handles = []
+
+    def allreduce_async(self, t: torch.Tensor) -> None:
+        if self.enabled:
+            self._handles.append(dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+
+    def wait(self) -> None:
+        for h in self._handles:
+            h.wait()
+        self._handles = []
+
+
+class FlatParams:
+    """All parameters of a model as views into one contiguous fp32 buffer, with a matching
+    flat gradient buffer.  Layer attributes are rebound to the views, so the layers (and the
+    drop-in autograd API) read the flat storage directly."""
+
+    def __init__(self, model: Model):
+        named = list(model.parameters().items())
+        dev = named[0][1].device
+        self.names = [n for n, _ in named]
+        self.numel = [p.numel() for _, p in named]
+        total = sum(self.numel)
+        self.data = torch.empty(total, device=dev, dtype=torch.float32)
+        self.grad = torch.zeros(total, device=dev, dtype=torch.float32)
+        self.views, self.gviews, self.offsets = {}, {}, {}
+        off = 0
+        for (name, p), n in zip(named, self.numel):
+            self.data[off:off + n].copy_(p.detach().reshape(-1))
+            self.views[name] = self.data[off:off + n].view(p.shape)
+            self.gviews[name] = self.grad[off:off + n].view(p.shape)
+            self.offsets[name] = (off, off + n)
+            off += n
+        for i, layer in enumerate(model.layers):
+            for pname in layer.parameters():
+                setattr(layer, pname, self.views[f"layer{i}.{pname}"])
+
+    def layer_slice(self, i: int, model: Model) -> tuple[int, int]:
+        names = [f"layer{i}.{p}" for p in model.layers[i].parameters()]
+        return min(self.offsets[n][0] for n in names), max(self.offsets[n][1] for n in names)
+
+
+class SplineTrainer:
+    """One-process-per-GPU data-parallel trainer for KAN / UKAN stacks."""
+
+    def __init__(self, model: Model, loss_kind: str, lr: float, optimizer: str = "adam",
+                 weight_decay: float = 0.0, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 group=None):
+        if model.kind not in ("kan", "ukan"):
+            raise ConfigError(f"SplineTrainer handles kan/ukan stacks, got {model.kind!r}")
+        if loss_kind not in ("mse", "softmax_cross_entropy"):
+            raise ConfigError(f"unknown loss kind {loss_kind!r}")
+        self.lib = _lib.load()
+        self.model = model
+        self.loss_kind = loss_kind
+        self.lr, self.optimizer, self.wd = lr, optimizer, weight_decay
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.flat = FlatParams(model)
+        self.sync = GradSync(group)
+        self.t = 0
+        dev = self.flat.data.device
+        self.m = torch.zeros_like(self.flat.data) if optimizer == "adam" else None
+        self.v = torch.zeros_like(self.flat.data) if optimizer == "adam" else None
+        self._loss_buf = None
+        self.device = dev
+        self.kernel_launches = 0
+
+    # -- per-layer forward / backward on raw buffers ------------------------------------
+    def _fwd(self, layer, h):
+        st = stream_ptr()
+        B = h.shape[0]
+        y = torch.empty((B, layer.d_out), device=self.device, dtype=torch.float32)
+        if isinstance(layer, KanLayer):
+            check(self.lib.ukan_kan_forward(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(layer.base_weight),
+                                            ptr(y), B, layer.d_in, layer.d_out, layer.G, layer.k,
+                                            float(layer.g_min), float(layer.g_max), ptr(self._err), st),
+                  "kan_forward")
+            self.kernel_launches += 1
+            return y, None
+        keys = ops.ukan_build_keys(h, layer.k, float(layer.delta_g))
+        self.kernel_launches += 5
+        n_u = keys.n_u
+        d_h = layer.cg_w1.shape[1]
+        d_cg = layer.cg_w1.shape[0]
+        n_out = layer.cg_w2.shape[1]
+        inp = torch.empty((n_u, d_cg), device=self.device, dtype=torch.float32)
+        pre = torch.empty((n_u, d_h), device=self.device, dtype=torch.float32)
+        H = torch.empty_like(pre)
+        table = torch.empty((n_u, n_out), device=self.device, dtype=torch.float32)
+        check(self.lib.ukan_ukan_cg_input(ptr(keys.key_f), ptr(keys.key_g), ptr(layer.feature_embedding), ptr(inp),
+                                          n_u, layer.d_femb, layer.d_pe, st), "cg_input")
+        check(self.lib.ukan_gemm_bias_act(ptr(inp), ptr(layer.cg_w1), ptr(layer.cg_b1), ptr(H), ptr(pre), n_u, d_h,
+                                          d_cg, 1, st), "cg_gemm1")
+        check(self.lib.ukan_gemm_bias_act(ptr(H), ptr(layer.cg_w2), ptr(layer.cg_b2), ptr(table), None, n_u, n_out,
+                                          d_h, 0, st), "cg_gemm2")
+        check(self.lib.ukan_ukan_forward(ptr(h), ptr(keys.base_row), ptr(table), ptr(layer.scale), ptr(y), B,
+                                         layer.d_in, layer.d_out, layer.k, float(layer.delta_g), st), "ukan_forward")
+        self.kernel_launches += 4
+        return y, (keys, inp, pre, H, table)
+
+    def _bwd(self, i, layer, h, gy, cache, need_dx):
+        st = stream_ptr()
+        B = h.shape[0]
+        pre_ = f"layer{i}."
+        gv = self.flat.gviews
+        dx = torch.empty_like(h) if need_dx else None
+        if isinstance(layer, KanLayer):
+            nbytes = self.lib.ukan_kan_backward_workspace_size(B, layer.d_in, layer.d_out, layer.G, layer.k)
+            ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8) if nbytes else None
+            bw = layer.base_weight
+            check(self.lib.ukan_kan_backward_ws(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(bw), ptr(gy),
+                                                ptr(dx), ptr(gv[pre_ + "coeffs"]), ptr(gv[pre_ + "scale"]),
+                                                ptr(gv.get(pre_ + "base_weight")) if bw is not None else None,
+                                                B, layer.d_in, layer.d_out, layer.G, layer.k, float(layer.g_min),
+                                                float(layer.g_max), ptr(ws), nbytes, st), "kan_backward")
+            self.kernel_launches += 2 if need_dx else 1
+            return dx
+        keys, inp, pre, H, table = cache
+        n_u = keys.n_u
+        d_h = H.shape[1]
+        d_cg = inp.shape[1]
+        n_out = table.shape[1]
+        dtable = torch.empty_like(table)
+        nbytes = self.lib.ukan_ukan_backward_workspace_size(B, layer.d_in, layer.d_out, n_u, layer.k)
+        ws = torch.empty(max(nbytes, 8), device=self.device, dtype=torch.uint8)
+        check(self.lib.ukan_ukan_backward(ptr(h), ptr(keys.base_row), ptr(keys.seg_start), ptr(table),
+                                          ptr(layer.scale), ptr(gy), ptr(dx), ptr(dtable), ptr(gv[pre_ + "scale"]),
+                                          B, layer.d_in, layer.d_out, n_u, layer.k, float(layer.delta_g), ptr(ws),
+                                          nbytes, st), "ukan_backward")
+        check(self.lib.ukan_gemm_tn(ptr(H), ptr(dtable), ptr(gv[pre_ + "cg_w2"]), ptr(gv[pre_ + "cg_b2"]), d_h, n_out,
+                                    n_u, st), "cg_dW2")
+        dH = torch.empty_like(H)
+        check(self.lib.ukan_gemm_nt(ptr(dtable), ptr(layer.cg_w2), ptr(dH), n_u, d_h, n_out, st), "cg_dH")
+        dpre = torch.empty_like(H)
+        check(self.lib.ukan_silu_backward(ptr(pre), ptr(dH), ptr(dpre), dH.numel(), st), "cg_dsilu")
+        check(self.lib.ukan_gemm_tn(ptr(inp), ptr(dpre), ptr(gv[pre_ + "cg_w1"]), ptr(gv[pre_ + "cg_b1"]), d_cg, d_h,
+                                    n_u, st), "cg_dW1")
+        dinp = torch.empty_like(inp)
+        check(self.lib.ukan_gemm_nt(ptr(dpre), ptr(layer.cg_w1), ptr(dinp), n_u, d_cg, d_h, st), "cg_dinp")
+        check(self.lib.ukan_ukan_emb_backward(ptr(keys.seg_start), ptr(dinp), ptr(gv[pre_ + "feature_embedding"]),
+                                              layer.d_in, layer.d_femb, d_cg, st), "cg_demb")
+        self.kernel_launches += 10 + (1 if need_dx else 0)
+        return dx
+
+    # -- the step --------------------------------------------------------------------------
+    def step(self, x: torch.Tensor, target: torch.Tensor, n_global: int | None = None, lr: float | None = None):
+        """One DP training step on this rank's shard (x, target already on the device).
+        Returns the device fp64 global loss (read it with ``read_loss``)."""
+        st = stream_ptr()
+        layers = self.model.layers
+        B = x.shape[0]
+        if n_global is None:
+            n_global = B * self.sync.world
+        self._err = torch.zeros(1, device=self.device, dtype=torch.int32)
+        hs = [x]
+        caches = []
+        for layer in layers:
+            y, cache = self._fwd(layer, hs[-1])
+            hs.append(y)
+            caches.append(cache)
+        out = hs[-1]
+        if self._loss_buf is None or self._loss_buf.numel() < out.numel() + 1:
+            self._loss_buf = torch.empty(out.numel() + 1, device=self.device, dtype=torch.float64)
+        gy = torch.empty_like(out)
+        if self.loss_kind == "softmax_cross_entropy":
+            check(self.lib.ukan_softmax_xent(ptr(out), ptr(target), ptr(self._loss_buf), ptr(gy), B, out.shape[1],
+                                             n_global, 1.0, st), "softmax_xent")
+        else:
+            n_el = out.numel()
+            check(self.lib.ukan_mse(ptr(out), ptr(target), ptr(self._loss_buf), ptr(gy), n_el,
+                                    n_el // B * n_global, st), "mse")
+        self.kernel_launches += 2
+        loss = self._loss_buf[:1]
+        self.sync.allreduce_async(loss)
+        for i in range(len(layers) - 1, -1, -1):
+            gy = self._bwd(i, layers[i], hs[i], gy, caches[i], need_dx=i > 0)
+            lo, hi = self.flat.layer_slice(i, self.model)
+            self.sync.allreduce_async(self.flat.grad[lo:hi])
+        self.sync.wait()
+        self.t += 1
+        lr = self.lr if lr is None else lr
+        n = self.flat.data.numel()
+        if self.optimizer == "adam":
+            check(self.lib.ukan_adam_step(ptr(self.flat.data), ptr(self.flat.grad), ptr(self.m), ptr(self.v), n, lr,
+                                          self.beta1, self.beta2, self.eps, self.wd, self.t, ptr(loss), st), "adam")
+        else:
+            check(self.lib.ukan_sgd_step(ptr(self.flat.data), ptr(self.flat.grad), n, lr, ptr(loss), st), "sgd")
+        self.kernel_launches += 1
+        return loss
+
+    def read_loss(self, loss: torch.Tensor) -> float:
+        """Host read of the step's loss; raises DivergedError / IndexError like the reference."""
+        v = float(loss.item())
+        if int(self._err.item()):
+            raise IndexError("non-finite (NaN) input to a bounded-grid KAN layer")
+        if not math.isfinite(v):
+            raise DivergedError(f"non-finite loss {v}")
+        return v
