@@ -13,6 +13,9 @@
 //   UKAN: T = CG output viewed as [n_u*K, d_out] (slot-major), row_bi = base_row[b,i]; with
 //         feature-major key order the K rows of a window are consecutive (see ukan_b200.h).
 // Each feature i owns a contiguous row segment [row0_i, row0_i + R_i) of T.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ukan {
@@ -471,6 +474,25 @@ __global__ void kan_locate_kernel(const float* __restrict__ x, int32_t* __restri
 // ---------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------
+struct RegPlan {
+  bool ok = false;
+  int rmax = 0, ov = 1, fpb = 1, wpf = 1, S = 1, sps = 0;
+  size_t smem = 0;
+  int64_t ws_bytes = 0;
+};
+RegPlan kan_bwd_reg_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base, int sms);
+template <int K>
+int kan_bwd_reg_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
+                         float* dscale, float* dbw, double* ws, int B, int d_in, int d_out, int R,
+                         const KanGrid& grid, const RegPlan& p, cudaStream_t st);
+template <int K>
+int kan_dx_narrow(const float* x, const float* C, const float* scale, const float* bw, const float* gy, float* dx,
+                  int B, int d_in, int d_out, int R, const KanGrid& grid, cudaStream_t st);
+int kan_num_sms();
+template <int K>
+int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
+               int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
+
 constexpr size_t kSmemCap = 220 * 1024;
 constexpr int kBwdOV = 2;
 
@@ -490,22 +512,36 @@ template <int K, bool UKAN>
 static int launch_fwd(const float* x, const float* T, const float* scale, const float* bw,
                       float* y, int B, int d_in, int d_out, const RowMap& rm, int32_t* err,
                       cudaStream_t st) {
+  if constexpr (!UKAN) {
+    // smem-slab variant (kan_fwd.cu): measured slower than this kernel at cfg2 (1.88 vs 1.68 ms,
+    // profiles/README.md), kept selectable for experiments via UKAN_FWD_V2=1
+    static const bool use_v2 = getenv("UKAN_FWD_V2") != nullptr;
+    if (use_v2) {
+      const int rc = kan_fwd_v2<K>(x, T, scale, bw, y, B, d_in, d_out, rm.R, rm.grid, err, st);
+      if (rc != UKAN_E_ARG) return rc;
+    }
+  }
   const Basis<K> bas = make_basis<K>(K - 1);
   const int VEC = (d_out % 4 == 0) ? 4 : (d_out % 2 == 0 ? 2 : 1);
   int TO = (d_out + VEC - 1) / VEC;
   if (TO > 32) TO = 32;
   int TS = 256 / TO;
   if (TS > 64) TS = 64;
+  {  // narrow layers: shrink the sample tile so the grid still covers ~2 waves
+    const int64_t otiles = (d_out + TO * VEC - 1) / (TO * VEC);
+    const int64_t want = 2 * (int64_t)kan_num_sms();
+    const int64_t ts_fit = ((int64_t)B + kFwdS * (want / otiles) - 1) / std::max<int64_t>(1, kFwdS * (want / otiles));
+    if (ts_fit < TS) TS = (int)std::max<int64_t>(1, ts_fit);
+  }
   const int Bt = TS * kFwdS;
   dim3 block(TO, TS);
   dim3 gridd((B + Bt - 1) / Bt, (d_out + TO * VEC - 1) / (TO * VEC));
   const size_t smem = (size_t)kFwdFC * Bt * (sizeof(int) + sizeof(float) * (K + 1));
-  if (VEC == 4)
-    spline_fwd_kernel<K, 4, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
-  else if (VEC == 2)
-    spline_fwd_kernel<K, 2, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
-  else
-    spline_fwd_kernel<K, 1, UKAN><<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
+  auto kern = VEC == 4 ? spline_fwd_kernel<K, 4, UKAN>
+                       : (VEC == 2 ? spline_fwd_kernel<K, 2, UKAN> : spline_fwd_kernel<K, 1, UKAN>);
+  if (smem > 48 * 1024)
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<gridd, block, smem, st>>>(x, T, scale, bw, y, B, d_in, d_out, rm, bas, err);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }
@@ -569,7 +605,7 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
                                 int32_t* err_flag, void* stream) {
   int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
   if (rc) return rc;
-  if (!x || !coeffs || !scale || !y) return UKAN_E_ARG;
+  if (!coeffs || !scale || (B > 0 && (!x || !y))) return UKAN_E_ARG;
   if (B == 0) return UKAN_OK;
   RowMap rm{};
   rm.grid = make_kan_grid(g_min, g_max, G);
@@ -581,10 +617,39 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
 
 extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
                                                     int64_t G, int k) {
-  (void)B;
-  if (k < 0 || k > UKAN_MAX_DEGREE || G < 1) return 0;
+  if (k < 0 || k > UKAN_MAX_DEGREE || G < 1 || B < 0 || d_in < 1 || d_out < 1) return 0;
+  const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, (int)(G + k), k + 1, true, kan_num_sms());
+  if (p.ok) return p.ws_bytes;
   if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
+}
+
+template <int K>
+static int kan_backward_impl(const float* x, const float* coeffs, const float* scale, const float* bw,
+                             const float* gy, float* dx, float* dC, float* dscale, float* dbw, void* workspace,
+                             int64_t workspace_bytes, int B, int d_in, int d_out, const RowMap& rm,
+                             cudaStream_t st) {
+  RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms());
+  if (!p.ok)
+    return launch_bwd<K, false>(x, coeffs, scale, bw, gy, dx, dC, dscale, dbw, (double*)workspace, B, d_in, d_out,
+                                rm.R, rm, st);
+  if (p.S > 1 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) {  // no workspace: one split
+    p.S = 1;
+    p.sps = B > 0 ? B : 1;
+  }
+  int rc = kan_bwd_reg_dispatch<K>(x, coeffs, scale, gy, dC, dscale, dbw, (double*)workspace, B, d_in, d_out, rm.R,
+                                   rm.grid, p, st);
+  if (rc) return rc;
+  if (dx && B > 0) {
+    if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+    const Basis<K> bas = make_basis<K>(K - 1);
+    const int64_t pairs = (int64_t)B * d_in;
+    const int wpb = 8;
+    spline_dx_kernel<K, false><<<(unsigned)((pairs + wpb - 1) / wpb), wpb * 32, 0, st>>>(
+        x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm, bas);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
 }
 
 extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,
@@ -595,15 +660,17 @@ extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const f
                                    int64_t workspace_bytes, void* stream) {
   int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
   if (rc) return rc;
-  if (!x || !coeffs || !scale || !gy || !dcoeffs || !dscale) return UKAN_E_ARG;
+  if (!coeffs || !scale || !dcoeffs || !dscale || (B > 0 && (!x || !gy))) return UKAN_E_ARG;
   if ((base_weight == nullptr) != (dbase_weight == nullptr)) return UKAN_E_ARG;
-  const int64_t need = ukan_kan_backward_workspace_size(B, d_in, d_out, G, k);
-  if (need > 0 && (workspace == nullptr || workspace_bytes < need)) return UKAN_E_WORKSPACE;
   RowMap rm{};
   rm.grid = make_kan_grid(g_min, g_max, G);
   rm.R = (int)(G + k);
+  const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, k + 1, base_weight != nullptr, kan_num_sms());
+  if (!p.ok && !bwd_fits_smem(k + 1, rm.R) &&
+      (workspace == nullptr || workspace_bytes < (int64_t)sizeof(double) * d_in * rm.R * d_out))
+    return UKAN_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  UKAN_DISPATCH_K(k, return launch_bwd<K, false>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, (double*)workspace, (int)B, (int)d_in, (int)d_out, rm.R, rm, st););
+  UKAN_DISPATCH_K(k, return kan_backward_impl<K>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out, rm, st););
   return UKAN_OK;
 }
 
@@ -635,7 +702,8 @@ extern "C" int ukan_ukan_forward(const float* x, const int32_t* base_row, const 
                                  int64_t d_out, int k, double delta_g, void* stream) {
   if (k < 0 || k > UKAN_MAX_DEGREE) return UKAN_E_DEGREE;
   if (!(delta_g > 0)) return UKAN_E_GRID;
-  if (!x || !base_row || !table || !scale || !y || B < 0 || d_in < 1 || d_out < 1 || B > INT32_MAX)
+  if (!table || !scale || B < 0 || d_in < 1 || d_out < 1 || B > INT32_MAX ||
+      (B > 0 && (!x || !base_row || !y)))
     return UKAN_E_ARG;
   if (B == 0) return UKAN_OK;
   RowMap rm{};

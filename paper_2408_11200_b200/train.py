@@ -109,6 +109,24 @@ class SplineTrainer:
         self._loss_buf = None
         self.device = dev
         self.kernel_launches = 0
+        self.timers = None  # optional {name: [(start_event, end_event), ...]} (bench.py)
+
+    def _mark(self, name):
+        """Record a CUDA event pair around one launch when timing is enabled."""
+        trainer = self
+
+        class _M:
+            def __enter__(self_):
+                if trainer.timers is not None:
+                    self_.a = torch.cuda.Event(enable_timing=True)
+                    self_.a.record()
+
+            def __exit__(self_, *exc):
+                if trainer.timers is not None:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record()
+                    trainer.timers.setdefault(name, []).append((self_.a, b))
+        return _M()
 
     # -- per-layer forward / backward on raw buffers ------------------------------------
     def _fwd(self, layer, h):
@@ -116,6 +134,7 @@ class SplineTrainer:
         B = h.shape[0]
         y = torch.empty((B, layer.d_out), device=self.device, dtype=torch.float32)
         if isinstance(layer, KanLayer):
+          with self._mark(f"layer{self._li}.kan_forward"):
             check(self.lib.ukan_kan_forward(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(layer.base_weight),
                                             ptr(y), B, layer.d_in, layer.d_out, layer.G, layer.k,
                                             float(layer.g_min), float(layer.g_max), ptr(self._err), st),
@@ -153,7 +172,8 @@ class SplineTrainer:
             nbytes = self.lib.ukan_kan_backward_workspace_size(B, layer.d_in, layer.d_out, layer.G, layer.k)
             ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8) if nbytes else None
             bw = layer.base_weight
-            check(self.lib.ukan_kan_backward_ws(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(bw), ptr(gy),
+            with self._mark(f"layer{i}.kan_backward"):
+              check(self.lib.ukan_kan_backward_ws(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(bw), ptr(gy),
                                                 ptr(dx), ptr(gv[pre_ + "coeffs"]), ptr(gv[pre_ + "scale"]),
                                                 ptr(gv.get(pre_ + "base_weight")) if bw is not None else None,
                                                 B, layer.d_in, layer.d_out, layer.G, layer.k, float(layer.g_min),
@@ -196,10 +216,15 @@ class SplineTrainer:
         B = x.shape[0]
         if n_global is None:
             n_global = B * self.sync.world
-        self._err = torch.zeros(1, device=self.device, dtype=torch.int32)
+        if getattr(self, "_err", None) is None:
+            self._err = torch.zeros(1, device=self.device, dtype=torch.int32)
+        else:  # reset the NaN flag with our fill kernel (0.0f has the all-zero bit pattern)
+            check(self.lib.ukan_fill_f32(ptr(self._err), 1, 0.0, st), "fill")
+            self.kernel_launches += 1
         hs = [x]
         caches = []
-        for layer in layers:
+        for li, layer in enumerate(layers):
+            self._li = li
             y, cache = self._fwd(layer, hs[-1])
             hs.append(y)
             caches.append(cache)
