@@ -17,6 +17,7 @@
 // that a second kernel reduces in fixed order (deterministic), so the grid fills 148 SMs.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -280,6 +281,219 @@ kan_bwd_reg_kernel(const float* __restrict__ x, const float* __restrict__ C,
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// FP64 tensor-core variant (cubic splines, K = 4): banded blocks on DMMA.
+//
+// The table gradient of one feature is a banded product A[r,o] = sum_b W[b,r] g[b,o] with
+// W[b, c_b .. c_b+3] = w(u_b).  Rows are covered by 8-row blocks with stride 4 (block bb =
+// rows 4bb .. 4bb+7), so every cell's 4-row window lies inside block c>>2.  Samples of a
+// 128-sample chunk are counting-sorted by cell per feature; consecutive groups of 4 sorted
+// samples form the K=4 operand of one `mma.sync.m8n8k4.f64` per 8-output tile
+// (D[8 rows x 8 outputs] += A[8 rows x 4 samples] B[4 samples x 8 outputs]), normally all four
+// in the same block.  Accumulators of block bb / tile nt live in registers (statically
+// indexed through a uniform unrolled block loop); each row is the sum of the two blocks that
+// contain it, reduced in fixed order at the end (deterministic).  IEEE fp64 products and sums.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int RB, int NT>
+__global__ void __launch_bounds__(256, 1)
+kan_bwd_dmma_kernel(const float* __restrict__ x, const float* __restrict__ C,
+                    const float* __restrict__ scale, const float* __restrict__ gy,
+                    float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
+                    int B, int d_in, int d_out, int R, int sps, KanGrid grid, Basis<4> bas, int dbg) {
+  constexpr int K = 4;
+  constexpr int FPB = 8;
+  constexpr int OPB = 8 * NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * FPB;
+  const int i = i0 + warp;
+  const int o0 = blockIdx.y * OPB;
+  const int z = blockIdx.z;
+  const int b_lo = z * sps, b_hi = min(B, b_lo + sps);
+  const int grp = lane >> 2, kq = lane & 3;
+
+  double* g64 = reinterpret_cast<double*>(smem_raw);             // [BC][OPB]
+  double* acol = g64 + (size_t)kRegBC * OPB;                      // [FPB][BC][8] A columns (sorted)
+  float* g_s0 = reinterpret_cast<float*>(acol + (size_t)FPB * kRegBC * 8);  // 2 x [BC][OPB]
+  float* x_s0 = g_s0 + (size_t)2 * kRegBC * OPB;                  // 2 x [BC][FPB]
+  int* csort = reinterpret_cast<int*>(x_s0 + 2 * kRegBC * FPB);   // [FPB][BC]
+  int* ent = csort + FPB * kRegBC;                                // [FPB][BC]
+  int* hist = ent + FPB * kRegBC;                                 // [FPB][2][4*RB + 8]
+
+  double acc[RB][NT][2];
+#pragma unroll
+  for (int bb = 0; bb < RB; ++bb)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[bb][t][0] = acc[bb][t][1] = 0.0;
+
+  const int nchunks = (b_hi - b_lo + kRegBC - 1) / kRegBC;
+  if (nchunks > 0) stage_chunk(g_s0, x_s0, gy, x, b_lo, min(kRegBC, b_hi - b_lo), o0, OPB, d_out, i0, FPB, d_in);
+  cp_async_commit();
+  for (int n = 0; n < nchunks; ++n) {
+    const int b0 = b_lo + n * kRegBC;
+    const int nb = min(kRegBC, b_hi - b0);
+    const float* g_s = g_s0 + (size_t)(n & 1) * kRegBC * OPB;
+    const float* x_s = x_s0 + (size_t)(n & 1) * kRegBC * FPB;
+    if (n + 1 < nchunks) {
+      const int b1 = b0 + kRegBC;
+      stage_chunk(g_s0 + (size_t)((n + 1) & 1) * kRegBC * OPB, x_s0 + (size_t)((n + 1) & 1) * kRegBC * FPB, gy,
+                  x, b1, min(kRegBC, b_hi - b1), o0, OPB, d_out, i0, FPB, d_in);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    for (int t = threadIdx.x; t < kRegBC * OPB; t += blockDim.x) g64[t] = (double)g_s[t];
+    // per feature (its warp): fp64 locate + basis of the chunk, stable counting sort by cell
+    constexpr int NB = 4 * RB + 8;  // histogram bins (cells 0 .. 4RB-1, +1 shift, padding)
+    int* st = hist + warp * 2 * NB;  // [NB] run starts, then [NB] scatter cursors
+    if (i < d_in && !(dbg & 2)) {
+      constexpr int PER = kRegBC / 32;
+      int* cur = st + NB;
+      for (int c = lane; c < NB; c += 32) cur[c] = 0;
+      __syncwarp();
+      int cells[PER];
+      double w[PER][K];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int s = q * 32 + lane;
+        int cell = -1;
+        double u = 0.0;
+        bool mask;
+        if (s < nb) kan_locate(x_s[s * FPB + warp], grid, cell, u, mask);
+        basis_weights<K>(bas, u, w[q]);
+        cells[q] = cell;
+        const unsigned m = __match_any_sync(0xffffffffu, cell);
+        if (cell >= 0 && lane == __ffs(m) - 1) cur[cell + 1] += __popc(m);
+        __syncwarp();
+      }
+      // warp-parallel inclusive scan of the shifted histogram -> start of each cell
+      int carry = 0;
+      for (int c0 = 0; c0 < NB; c0 += 32) {
+        const int c = c0 + lane;
+        int v = c < NB ? cur[c] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v, off);
+          if (lane >= off) v += t;
+        }
+        v += carry;
+        if (c < NB) {
+          st[c] = v;
+          cur[c] = v;
+        }
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int cell = cells[q];
+        const unsigned m = __match_any_sync(0xffffffffu, cell);
+        int base = 0;
+        if (cell >= 0) base = cur[cell];
+        __syncwarp();
+        if (cell >= 0) {
+          const int pos = base + __popc(m & ((1u << lane) - 1u));
+          ent[warp * kRegBC + pos] = (q * 32 + lane) * OPB;  // g64 row offset of the sample
+          csort[warp * kRegBC + pos] = cell;
+          // the sample's column of the 8-row block (cell >> 2): weights at rows (cell & 3) + j
+          double* ac = acol + ((size_t)warp * kRegBC + pos) * 8;
+          const int sh = cell & 3;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int j = r - sh;
+            ac[r] = (j == 0) ? w[q][0] : (j == 1) ? w[q][1] : (j == 2) ? w[q][2] : (j == 3) ? w[q][3] : 0.0;
+          }
+          if (lane == __ffs(m) - 1) cur[cell] = base + __popc(m);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // sweep: block bb (rows 4bb..4bb+7) takes the sorted samples of cells 4bb..4bb+3, four at a
+    // time, one DMMA per 8-output tile into the statically indexed accumulators acc[bb][t];
+    // the operands of the next group are loaded before the current group's DMMAs issue
+    if (i < d_in && !(dbg & 1)) {
+      const int* es = ent + warp * kRegBC;
+      const double* ac = acol + (size_t)warp * kRegBC * 8 + grp;
+      const double* gl = g64 + grp;
+#pragma unroll
+      for (int bb = 0; bb < RB; ++bb) {
+        const int e0 = st[4 * bb], e1 = st[4 * bb + 4];
+        if (e0 >= e1) continue;
+        int pos = e0 + kq;
+        bool vld = pos < e1;
+        double a_n = vld ? ac[pos * 8] : 0.0;
+        int so = es[pos];
+        double b_n[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) b_n[t] = vld ? gl[so + t * 8] : 0.0;
+        for (int kc = e0; kc < e1; kc += 4) {
+          const double a = a_n;
+          double bf[NT];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) bf[t] = b_n[t];
+          pos += 4;
+          vld = pos < e1;
+          a_n = vld ? ac[min(pos, kRegBC - 1) * 8] : 0.0;
+          so = es[min(pos, kRegBC - 1)];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) b_n[t] = vld ? gl[so + t * 8] : 0.0;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma_884(acc[bb][t][0], acc[bb][t][1], a, bf[t]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (i >= d_in) return;
+  // rows 4bb..4bb+3 = lower half of block bb (lanes 0..15) + upper half of block bb-1
+  // (lanes 16..31 of block bb-1, moved down by 16 lanes); fixed order -> deterministic
+  double ds[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) ds[t][0] = ds[t][1] = 0.0;
+#pragma unroll
+  for (int bb = 0; bb <= RB; ++bb) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const double lower = bb < RB ? acc[bb][t][v] : 0.0;
+        const double upper = bb > 0 ? __shfl_down_sync(0xffffffffu, acc[bb - 1][t][v], 16) : 0.0;
+        const double a = lower + upper;
+        const int r = 4 * bb + grp;
+        const int o = o0 + t * 8 + 2 * kq + v;
+        if (lane < 16 && r < R && o < d_out) {
+          const size_t ci = ((size_t)i * R + r) * d_out + o;
+          if (part != nullptr) {
+            part[(size_t)z * d_in * R * d_out + ci] = a;
+          } else {
+            dC[ci] = (float)((double)scale[(size_t)i * d_out + o] * a);
+            ds[t][v] = fma((double)C[ci], a, ds[t][v]);
+          }
+        }
+      }
+    }
+  }
+  if (part == nullptr) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double d = ds[t][v];
+        d += __shfl_xor_sync(0xffffffffu, d, 4);
+        d += __shfl_xor_sync(0xffffffffu, d, 8);
+        const int o = o0 + t * 8 + 2 * kq + v;
+        if (lane < 4 && o < d_out) dscale[(size_t)i * d_out + o] = (float)d;
+      }
+  }
+}
+
 // Fixed-order reduction of the split-batch partials + epilogue.  Thread per (i, o).
 __global__ void kan_bwd_reduce_kernel(const double* __restrict__ part, const double* __restrict__ part_b,
                                       const float* __restrict__ C, const float* __restrict__ scale,
@@ -454,6 +668,77 @@ int kan_dx_narrow(const float* x, const float* C, const float* scale, const floa
 }
 
 int kan_num_sms() { return num_sms(); }
+
+// DMMA path: cubic splines without the base branch, G <= 64.
+bool kan_bwd_dmma_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base, int sms, RegPlan& p) {
+  if (K != 4 || has_base) return false;
+  const int G = R - K + 1;
+  const int rbn = ((G - 1) >> 2) + 1;
+  int rb = 0;
+  if (rbn <= 4) rb = 4;
+  else if (rbn <= 8) rb = 8;
+  else if (rbn <= 16) rb = 16;
+  else return false;
+  const int nt = rb == 16 ? 2 : (d_out <= 8 ? 1 : (d_out <= 16 ? 2 : 4));
+  p.rmax = rb;
+  p.ov = nt;
+  p.fpb = 8;
+  p.wpf = 1;
+  const int opb = 8 * nt;
+  p.smem = sizeof(double) * ((size_t)kRegBC * opb + (size_t)8 * kRegBC * 8) + sizeof(float) * (size_t)2 * kRegBC * (opb + 8) +
+           sizeof(int) * ((size_t)2 * 8 * kRegBC + (size_t)8 * 2 * (4 * rb + 8));
+  const int64_t base = ((d_in + 7) / 8) * ((d_out + opb - 1) / opb);
+  int64_t S = 1;
+  if (base < 2 * (int64_t)sms) {
+    const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(16, B / (4 * kRegBC)));
+    double best = -1.0;
+    for (int64_t c = 1; c <= max_s; ++c) {
+      const double waves = (double)(base * c) / sms;
+      const double eff = waves / std::ceil(waves) * std::min(1.0, waves / 2.0);
+      if (eff > best + 1e-9) { best = eff; S = c; }
+    }
+  }
+  p.sps = (int)(((B + S - 1) / S + kRegBC - 1) / kRegBC * kRegBC);
+  if (p.sps == 0) p.sps = kRegBC;
+  p.S = (int)std::max<int64_t>(1, (B + p.sps - 1) / p.sps);
+  p.ws_bytes = p.S > 1 ? (int64_t)sizeof(double) * p.S * d_in * (int64_t)d_out * R : 0;
+  p.ok = true;
+  return true;
+}
+
+template <int RB, int NT>
+static int launch_dmma(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                       double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid, const RegPlan& p,
+                       cudaStream_t st) {
+  const Basis<4> bas = make_basis<4>(3);
+  auto kern = kan_bwd_dmma_kernel<RB, NT>;
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 gridd((d_in + 7) / 8, (d_out + 8 * NT - 1) / (8 * NT), p.S);
+  double* part = p.S > 1 ? ws : nullptr;
+  static const int dbg = getenv("UKAN_DBG") ? atoi(getenv("UKAN_DBG")) : 0;  // profiling knobs only
+  kern<<<gridd, 256, p.smem, st>>>(x, C, scale, gy, dC, dscale, part, B, d_in, d_out, R, p.sps, grid, bas, dbg);
+  UKAN_LAUNCH_CHECK();
+  if (p.S > 1) {
+    const int64_t n = (int64_t)d_in * d_out;
+    kan_bwd_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nullptr, C, scale, dC, dscale, nullptr,
+                                                                       p.S, d_in, d_out, R);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
+
+int kan_bwd_dmma_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
+                          float* dscale, double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid,
+                          const RegPlan& p, cudaStream_t st) {
+  if (p.rmax == 4 && p.ov == 1) return launch_dmma<4, 1>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 4 && p.ov == 2) return launch_dmma<4, 2>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 4) return launch_dmma<4, 4>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 8 && p.ov == 1) return launch_dmma<8, 1>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 8 && p.ov == 2) return launch_dmma<8, 2>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 8) return launch_dmma<8, 4>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  if (p.rmax == 16) return launch_dmma<16, 2>(x, C, scale, gy, dC, dscale, ws, B, d_in, d_out, R, grid, p, st);
+  return UKAN_E_ARG;
+}
 
 #define UKAN_INST(K)                                                                                            \
   template int kan_bwd_reg_dispatch<K>(const float*, const float*, const float*, const float*, float*, float*,   \

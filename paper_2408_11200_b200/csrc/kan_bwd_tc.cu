@@ -1,0 +1,382 @@
+// kan_bwd_tc.cu — KAN backward (table side) for cubic splines on the FP64 tensor cores.
+//
+// Replaces the bwd closures of span_gather (layers.py:67-70, the np.add.at scatter of the window
+// gradient) and edge_combine (84-88) for k = 3 without the base branch:
+//   A[i,r,o] = sum_{(b,j): cell_bi + j = r} w_j(u_bi) * g[b,o]     (fp64)
+//   dC = scale * A,   dscale = sum_r C * A.
+//
+// Two kernels.
+//  * prep: once per (feature, 128-sample chunk) — fp64 locate with the reference's expression
+//    order (layers.py:299-300), stable counting sort of the chunk by cell, record
+//    {(cell<<8)|sample, u} in cell order plus the start of every cell.  The records of a layer
+//    (~14 B per (sample, feature)) stay L2-resident and are shared by every output tile.
+//  * sweep: a CTA owns 8 features x 8*NT outputs; per chunk it stages (cp.async, double
+//    buffered) the 8 feature records and g[chunk, o-tile].  Rows are covered by 8-row blocks
+//    with stride 4 (block bb = rows 4bb..4bb+7), so a cell's 4-row window lies in block cell>>2.
+//    Four consecutive sorted samples of cells 4bb..4bb+3 form the k=4 operand of one
+//    `mma.sync.m8n8k4.f64` (DMMA) per 8-output tile:
+//        D[8 rows x 8 out] += A[8 rows x 4 samples] * B[4 samples x 8 out],
+//    A[r][k] = w_{r - (cell_k & 3)}(u_k) (evaluated in-lane from u, fp64 Horner),
+//    B[k][n] = g[sample_k][o_n].  Accumulators acc[bb][t] are statically indexed registers;
+//    each row is the sum of the two blocks holding it, reduced in fixed order at the end.
+// Deterministic: fixed sample order per chunk, fixed chunk order, fixed reductions.  IEEE fp64
+// products and sums throughout.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace ukan {
+
+constexpr int kTcBC = 128;  // samples per chunk
+
+// prep record layout (bytes, 16-aligned): ent[128] int | u[128] double | st[NBP] int
+__host__ __device__ constexpr int tc_nbp(int G) { return ((G + 1 + 3) / 4) * 4; }
+__host__ __device__ constexpr size_t tc_rec_bytes(int G) {
+  return (size_t)kTcBC * 4 + (size_t)kTcBC * 8 + (size_t)tc_nbp(G) * 4;
+}
+
+__global__ void __launch_bounds__(256)
+kan_bwd_tc_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ recs, int B, int d_in,
+                       int nch, int G, KanGrid grid) {
+  __shared__ float xs[kTcBC][9];
+  __shared__ int cnt[8][80];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * 8;
+  const int n = blockIdx.y;
+  const int b0 = n * kTcBC;
+  const int nb = min(kTcBC, B - b0);
+  for (int t = threadIdx.x; t < kTcBC * 8; t += blockDim.x) {
+    const int s = t / 8, f = t % 8;
+    xs[s][f] = (s < nb && i0 + f < d_in) ? x[(size_t)(b0 + s) * d_in + i0 + f] : 0.f;
+  }
+  __syncthreads();
+  const int i = i0 + warp;
+  if (i >= d_in) return;
+  const size_t rb = tc_rec_bytes(G);
+  unsigned char* rec = recs + ((size_t)i * nch + n) * rb;
+  int* ent = reinterpret_cast<int*>(rec);
+  double* uu = reinterpret_cast<double*>(rec + kTcBC * 4);
+  int* st = reinterpret_cast<int*>(rec + kTcBC * 12);
+  const int NB = G + 1;
+  // shared cursor space: G+1 <= 80 handled here (G <= 64 on this path)
+  int* cur = cnt[warp];
+  for (int c = lane; c < NB + 1; c += 32) cur[c] = 0;
+  __syncwarp();
+  constexpr int PER = kTcBC / 32;
+  int cells[PER];
+  double us[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int s = q * 32 + lane;
+    int cell = -1;
+    double u = 0.0;
+    bool mask;
+    if (s < nb) kan_locate(xs[s][warp], grid, cell, u, mask);
+    cells[q] = cell;
+    us[q] = u;
+    const unsigned m = __match_any_sync(0xffffffffu, cell);
+    if (cell >= 0 && lane == __ffs(m) - 1) cur[cell + 1] += __popc(m);
+    __syncwarp();
+  }
+  // inclusive scan of the shifted histogram -> start of each cell (cur[c]); st[] copy
+  int carry = 0;
+  for (int c0 = 0; c0 < NB; c0 += 32) {
+    const int c = c0 + lane;
+    int v = c < NB ? cur[c] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += t;
+    }
+    v += carry;
+    if (c < NB) {
+      cur[c] = v;
+      st[c] = v;
+    }
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
+  for (int c = NB + lane; c < tc_nbp(G); c += 32) st[c] = nb;
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int cell = cells[q];
+    const unsigned m = __match_any_sync(0xffffffffu, cell);
+    int base = 0;
+    if (cell >= 0) base = cur[cell];
+    __syncwarp();
+    if (cell >= 0) {
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      ent[pos] = (cell << 8) | (q * 32 + lane);
+      uu[pos] = us[q];
+      if (lane == __ffs(m) - 1) cur[cell] = base + __popc(m);
+    }
+    __syncwarp();
+  }
+  // tail positions (partial last chunk): harmless padding
+  for (int p = nb + lane; p < kTcBC; p += 32) {
+    ent[p] = 0;
+    uu[p] = 0.0;
+  }
+}
+
+__device__ __forceinline__ void tc_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void tc_cp16(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void tc_cp4(void* smem, const void* gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(ok ? 4 : 0));
+}
+
+template <int RB, int NT>
+__global__ void __launch_bounds__(256, 1)
+kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
+                        const float* __restrict__ scale, const float* __restrict__ gy,
+                        float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
+                        int B, int d_in, int d_out, int G, int nch, int cps, Basis<4> bas) {
+  constexpr int OPB = 8 * NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  const int i0 = blockIdx.x * 8;
+  const int i = i0 + warp;
+  const int o0 = blockIdx.y * OPB;
+  const int z = blockIdx.z;
+  const int n_lo = z * cps, n_hi = min(nch, n_lo + cps);
+  const int R = G + 3;
+  const size_t rb = tc_rec_bytes(G);
+  __shared__ double Msh[16];  // basis matrix (dynamic column index -> shared, not local memory)
+  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  unsigned char* rec_s = smem_raw;                                            // 2 x [8][rb]
+  float* g_s = reinterpret_cast<float*>(smem_raw + 2 * 8 * rb);               // 2 x [BC][OPB]
+
+  auto stage = [&](int n, int buf) {
+    // feature records (contiguous, 16-byte granules)
+    unsigned char* dst = rec_s + (size_t)buf * 8 * rb;
+    const int q = (int)(rb / 16);
+    for (int t = threadIdx.x; t < 8 * q; t += blockDim.x) {
+      const int f = t / q, c = t % q;
+      const bool ok = i0 + f < d_in;
+      const unsigned char* src = ok ? recs + ((size_t)(i0 + f) * nch + n) * rb + (size_t)c * 16 : recs;
+      tc_cp16(dst + (size_t)f * rb + (size_t)c * 16, src, ok ? 16 : 0);
+    }
+    // g[chunk, o-tile]
+    float* gd = g_s + (size_t)buf * kTcBC * OPB;
+    const int b0 = n * kTcBC;
+    const int nb = min(kTcBC, B - b0);
+    if ((d_out & 3) == 0) {
+      constexpr int q4 = OPB / 4;
+      for (int t = threadIdx.x; t < kTcBC * q4; t += blockDim.x) {
+        const int s = t / q4, oc = (t % q4) * 4;
+        const int o = o0 + oc;
+        const int bytes = (s < nb) ? max(0, min(4, d_out - o)) * 4 : 0;
+        tc_cp16(gd + s * OPB + oc, bytes ? gy + (size_t)(b0 + s) * d_out + o : gy, bytes);
+      }
+    } else {
+      for (int t = threadIdx.x; t < kTcBC * OPB; t += blockDim.x) {
+        const int s = t / OPB, oc = t % OPB;
+        const bool ok = s < nb && o0 + oc < d_out;
+        tc_cp4(gd + t, ok ? gy + (size_t)(b0 + s) * d_out + o0 + oc : gy, ok);
+      }
+    }
+  };
+
+  double acc[RB][NT][2];
+#pragma unroll
+  for (int bb = 0; bb < RB; ++bb)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[bb][t][0] = acc[bb][t][1] = 0.0;
+
+  if (n_lo < n_hi) stage(n_lo, 0);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int n = n_lo; n < n_hi; ++n) {
+    const int buf = (n - n_lo) & 1;
+    if (n + 1 < n_hi) stage(n + 1, buf ^ 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    if (i < d_in) {
+      const unsigned char* rec = rec_s + ((size_t)buf * 8 + warp) * rb;
+      const int* ent = reinterpret_cast<const int*>(rec);
+      const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
+      const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
+      const float* gl = g_s + (size_t)buf * kTcBC * OPB + grp;
+#pragma unroll
+      for (int bb = 0; bb < RB; ++bb) {
+        const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
+#pragma unroll 2
+        for (int kc = e0; kc < e1; kc += 4) {
+          const int pos = kc + kq;
+          const bool vld = pos < e1;
+          const int e = ent[min(pos, kTcBC - 1)];
+          const double u = uu[min(pos, kTcBC - 1)];
+          const int j = grp - ((e >> 8) & 3);
+          double a = 0.0;
+          if (vld && j >= 0 && j < 4) {  // w_j(u) = sum_m M[m][j] u^m  (Horner, fp64)
+            a = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+          }
+          const int srow = (e & 255) * OPB;
+          double bf[NT];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) bf[t] = vld ? (double)gl[srow + t * 8] : 0.0;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) tc_dmma(acc[bb][t][0], acc[bb][t][1], a, bf[t]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (i >= d_in) return;
+  double ds[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) ds[t][0] = ds[t][1] = 0.0;
+#pragma unroll
+  for (int bb = 0; bb <= RB; ++bb) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const double lower = bb < RB ? acc[bb][t][v] : 0.0;
+        const double upper = bb > 0 ? __shfl_down_sync(0xffffffffu, acc[bb - 1][t][v], 16) : 0.0;
+        const double a = lower + upper;
+        const int r = 4 * bb + grp;
+        const int o = o0 + t * 8 + 2 * kq + v;
+        if (lane < 16 && r < R && o < d_out) {
+          const size_t ci = ((size_t)i * R + r) * d_out + o;
+          if (part != nullptr) {
+            part[(size_t)z * d_in * R * d_out + ci] = a;
+          } else {
+            dC[ci] = (float)((double)scale[(size_t)i * d_out + o] * a);
+            ds[t][v] = fma((double)C[ci], a, ds[t][v]);
+          }
+        }
+      }
+    }
+  }
+  if (part == nullptr) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double d = ds[t][v];
+        d += __shfl_xor_sync(0xffffffffu, d, 4);
+        d += __shfl_xor_sync(0xffffffffu, d, 8);
+        const int o = o0 + t * 8 + 2 * kq + v;
+        if (lane < 4 && o < d_out) dscale[(size_t)i * d_out + o] = (float)d;
+      }
+  }
+}
+
+__global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const float* __restrict__ C,
+                                         const float* __restrict__ scale, float* __restrict__ dC,
+                                         float* __restrict__ dscale, int S, int d_in, int d_out, int R) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)d_in * d_out) return;
+  const int i = (int)(t / d_out), o = (int)(t % d_out);
+  const double sc = (double)scale[t];
+  const size_t zs = (size_t)d_in * R * d_out;
+  double ds = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const size_t ci = ((size_t)i * R + r) * d_out + o;
+    double a = 0.0;
+    for (int z = 0; z < S; ++z) a += part[z * zs + ci];
+    dC[ci] = (float)(sc * a);
+    ds = fma((double)C[ci], a, ds);
+  }
+  dscale[t] = (float)ds;
+}
+
+// ---------------------------------------------------------------------------------------
+struct TcPlan {
+  bool ok = false;
+  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0;
+  size_t smem = 0;
+  int64_t rec_bytes = 0, part_bytes = 0;
+};
+
+static int tc_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;
+  }
+  return n;
+}
+
+TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base) {
+  TcPlan p;
+  if (k != 3 || has_base || G < 1 || G > 64 || B < 1) return p;
+  const int rbn = (int)((G - 1) >> 2) + 1;
+  p.rb = rbn <= 4 ? 4 : (rbn <= 8 ? 8 : 16);
+  p.nt = p.rb == 16 ? 2 : (d_out <= 8 ? 1 : (d_out <= 16 ? 2 : 4));
+  const int opb = 8 * p.nt;
+  p.nch = (int)((B + kTcBC - 1) / kTcBC);
+  p.smem = 2 * 8 * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * opb;
+  p.rec_bytes = (int64_t)d_in * p.nch * (int64_t)tc_rec_bytes((int)G);
+  const int sms = tc_sms();
+  const int64_t base = ((d_in + 7) / 8) * ((d_out + opb - 1) / opb);
+  int64_t S = 1;
+  if (base < 2 * (int64_t)sms) {
+    const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(16, p.nch / 4));
+    double best = -1.0;
+    for (int64_t c = 1; c <= max_s; ++c) {
+      const double waves = (double)(base * c) / sms;
+      const double eff = waves / std::ceil(waves) * std::min(1.0, waves / 2.0);
+      if (eff > best + 1e-9) { best = eff; S = c; }
+    }
+  }
+  p.cps = (int)((p.nch + S - 1) / S);
+  p.S = (p.nch + p.cps - 1) / p.cps;
+  p.part_bytes = p.S > 1 ? (int64_t)sizeof(double) * p.S * d_in * d_out * (G + 3) : 0;
+  p.ok = true;
+  return p;
+}
+
+int64_t kan_bwd_tc_workspace(const TcPlan& p) { return p.ok ? ((p.rec_bytes + 255) / 256) * 256 + p.part_bytes : 0; }
+
+template <int RB, int NT>
+static int tc_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                     unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
+                     cudaStream_t st) {
+  auto kern = kan_bwd_tc_sweep_kernel<RB, NT>;
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 gridd((d_in + 7) / 8, (d_out + 8 * NT - 1) / (8 * NT), p.S);
+  kern<<<gridd, 256, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
+                                   p.nch, p.cps, make_basis<4>(3));
+  UKAN_LAUNCH_CHECK();
+  if (p.S > 1) {
+    const int64_t n = (int64_t)d_in * d_out;
+    kan_bwd_tc_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, C, scale, dC, dscale, p.S, d_in,
+                                                                          d_out, G + 3);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
+
+int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                   void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
+                   const TcPlan& p, cudaStream_t st) {
+  if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
+  unsigned char* recs = reinterpret_cast<unsigned char*>(workspace);
+  double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
+  dim3 pg((d_in + 7) / 8, p.nch);
+  kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid);
+  UKAN_LAUNCH_CHECK();
+  if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 4) return tc_launch<4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 8 && p.nt == 1) return tc_launch<8, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 8 && p.nt == 2) return tc_launch<8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 8) return tc_launch<8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.rb == 16) return tc_launch<16, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  return UKAN_E_ARG;
+}
+
+}  // namespace ukan

@@ -489,6 +489,21 @@ template <int K>
 int kan_dx_narrow(const float* x, const float* C, const float* scale, const float* bw, const float* gy, float* dx,
                   int B, int d_in, int d_out, int R, const KanGrid& grid, cudaStream_t st);
 int kan_num_sms();
+struct TcPlan {
+  bool ok = false;
+  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0;
+  size_t smem = 0;
+  int64_t rec_bytes = 0, part_bytes = 0;
+};
+TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
+int64_t kan_bwd_tc_workspace(const TcPlan& p);
+int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                   void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
+                   const TcPlan& p, cudaStream_t st);
+bool kan_bwd_dmma_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base, int sms, RegPlan& p);
+int kan_bwd_dmma_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
+                          float* dscale, double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid,
+                          const RegPlan& p, cudaStream_t st);
 template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
@@ -618,8 +633,11 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
 extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
                                                     int64_t G, int k) {
   if (k < 0 || k > UKAN_MAX_DEGREE || G < 1 || B < 0 || d_in < 1 || d_out < 1) return 0;
+  RegPlan dp;
+  const bool dm = kan_bwd_dmma_plan(B, d_in, d_out, (int)(G + k), k + 1, false, kan_num_sms(), dp);
   const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, (int)(G + k), k + 1, true, kan_num_sms());
-  if (p.ok) return p.ws_bytes;
+  const int64_t tc = kan_bwd_tc_workspace(kan_bwd_tc_plan(B, d_in, d_out, G, k, false));
+  if (p.ok) return std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc);
   if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
 }
@@ -629,7 +647,28 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
                              const float* gy, float* dx, float* dC, float* dscale, float* dbw, void* workspace,
                              int64_t workspace_bytes, int B, int d_in, int d_out, const RowMap& rm,
                              cudaStream_t st) {
-  RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms());
+  static const bool no_tc = getenv("UKAN_NO_TC") != nullptr;
+  if (!no_tc && K == 4 && bw == nullptr && B > 0) {  // FP64 tensor-core path (kan_bwd_tc.cu)
+    const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, rm.R - K + 1, K - 1, false);
+    if (tp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_tc_workspace(tp)) {
+      int rc = kan_bwd_tc_run(x, coeffs, scale, gy, dC, dscale, workspace, workspace_bytes, B, d_in, d_out,
+                              rm.R - K + 1, rm.grid, tp, st);
+      if (rc) return rc;
+      if (dx) {
+        if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+        const Basis<K> bas = make_basis<K>(K - 1);
+        const int64_t pairs = (int64_t)B * d_in;
+        spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
+                                                                               d_out, rm, bas);
+        UKAN_LAUNCH_CHECK();
+      }
+      return UKAN_OK;
+    }
+  }
+  RegPlan p;
+  static const bool no_dmma = getenv("UKAN_NO_DMMA") != nullptr;
+  const bool dm = !no_dmma && kan_bwd_dmma_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms(), p);
+  if (!dm) p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms());
   if (!p.ok)
     return launch_bwd<K, false>(x, coeffs, scale, bw, gy, dx, dC, dscale, dbw, (double*)workspace, B, d_in, d_out,
                                 rm.R, rm, st);
@@ -637,8 +676,10 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
     p.S = 1;
     p.sps = B > 0 ? B : 1;
   }
-  int rc = kan_bwd_reg_dispatch<K>(x, coeffs, scale, gy, dC, dscale, dbw, (double*)workspace, B, d_in, d_out, rm.R,
-                                   rm.grid, p, st);
+  int rc = dm ? kan_bwd_dmma_dispatch(x, coeffs, scale, gy, dC, dscale, (double*)workspace, B, d_in, d_out, rm.R,
+                                      rm.grid, p, st)
+              : kan_bwd_reg_dispatch<K>(x, coeffs, scale, gy, dC, dscale, dbw, (double*)workspace, B, d_in, d_out,
+                                        rm.R, rm.grid, p, st);
   if (rc) return rc;
   if (dx && B > 0) {
     if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);

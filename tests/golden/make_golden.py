@@ -163,3 +163,20 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def make_checkpoint_golden():
+    """A checkpoint written by the reference's own save_checkpoint (checkpoint.py:53-66)."""
+    sys.path.insert(0, REF)
+    from ukan.checkpoint import save_checkpoint
+    from ukan.config import RunConfig
+    from ukan.layers import build_model
+    model = build_model("kan", [3, 4, 2], 3, seed=5, G=6)
+    tensors = {n: f32(p.values) for n, p in model.parameters().items()}
+    cfg = RunConfig(model="kan", widths=[3, 4, 2], grid_size=6)
+    save_checkpoint(os.path.join(HERE, "ref_checkpoint.ukanckp"), cfg, tensors, {"epoch": 7, "adam_t": 3})
+    print("ref_checkpoint.ukanckp written")
+
+
+if __name__ == "__main__" and "--checkpoint" in sys.argv:
+    make_checkpoint_golden()

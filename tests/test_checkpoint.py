@@ -1,0 +1,55 @@
+"""UKANCKP1 interop: read a checkpoint written by the reference's own
+save_checkpoint, and write byte-identical files."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+import paper_2408_11200_b200 as P
+from paper_2408_11200_b200 import checkpoint as ck
+from paper_2408_11200_b200.errors import FormatError
+
+REF_CKPT = os.path.join(GOLDEN, "ref_checkpoint.ukanckp")
+
+
+def test_reads_reference_checkpoint_and_rewrites_identically(tmp_path):
+    cfg, tensors, meta = ck.load_checkpoint(REF_CKPT)
+    assert meta == {"adam_t": 3, "epoch": 7}
+    assert "model = kan" in cfg and "widths = 3,4,2" in cfg
+    assert list(tensors) == ["layer0.coeffs", "layer0.scale", "layer1.coeffs", "layer1.scale"]
+    out = tmp_path / "again.ukanckp"
+    ck.save_checkpoint(str(out), tensors, meta, cfg)
+    assert out.read_bytes() == open(REF_CKPT, "rb").read()
+
+
+def test_model_roundtrip_through_reference_format(tmp_path):
+    _, tensors, _ = ck.load_checkpoint(REF_CKPT)
+    model = P.build_model("kan", [3, 4, 2], 3, seed=0, G=6, device="cpu")
+    ck.load_model_state(model, tensors)
+    state = ck.model_state(model)
+    for n in tensors:
+        np.testing.assert_array_equal(state[n], tensors[n])   # values are fp32-representable
+    p = tmp_path / "m.ukanckp"
+    ck.save_checkpoint(str(p), state, {"epoch": 1})
+    _, t2, m2 = ck.load_checkpoint(str(p))
+    assert m2 == {"epoch": 1} and all(np.array_equal(t2[n], state[n]) for n in state)
+
+
+def test_format_errors(tmp_path):
+    bad = tmp_path / "bad"
+    bad.write_bytes(b"NOTACKPT" + b"\x01")
+    with pytest.raises(FormatError):
+        ck.load_checkpoint(str(bad))
+    data = open(REF_CKPT, "rb").read()
+    (tmp_path / "trunc").write_bytes(data[:-5])
+    with pytest.raises(FormatError):
+        ck.load_checkpoint(str(tmp_path / "trunc"))
+    (tmp_path / "trail").write_bytes(data + b"x")
+    with pytest.raises(FormatError):
+        ck.load_checkpoint(str(tmp_path / "trail"))
+    model = P.build_model("kan", [3, 5, 2], 3, seed=0, G=6, device="cpu")
+    _, tensors, _ = ck.load_checkpoint(REF_CKPT)
+    with pytest.raises(FormatError):
+        ck.load_model_state(model, tensors)
