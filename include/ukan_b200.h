@@ -57,6 +57,16 @@ int ukan_kan_forward(const float* x, const float* coeffs, const float* scale,
                      int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
                      double g_min, double g_max, int32_t* err_flag, void* stream);
 
+/* Same as ukan_kan_forward with a caller-provided device workspace (needed when the batch is
+ * too small to fill the GPU and d_in is split across CTAs: fp32 partial outputs, reduced in
+ * fixed order).  ukan_kan_forward itself takes it from a stream-ordered allocation. */
+int64_t ukan_kan_forward_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k);
+int ukan_kan_forward_ws(const float* x, const float* coeffs, const float* scale,
+                        const float* base_weight, float* y,
+                        int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
+                        double g_min, double g_max, int32_t* err_flag,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Backward of ukan_kan_forward given gy = dL/dy [B, d_out].  Replaces the bwd closures of
  * span_gather (layers.py:67-70), basis_features (44-46), edge_combine (84-88), clamp
  * (tensor.py:330-333) and the base branch.  dx [B, d_in] may be NULL (x not a recorded node,

@@ -35,6 +35,8 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_version": (_INT, []),
     "ukan_basis_matrix": (_INT, [_INT, _P]),
     "ukan_kan_forward": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _P]),
+    "ukan_kan_forward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),
+    "ukan_kan_forward_ws": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _P, _I64, _P]),
     "ukan_kan_backward": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT,
                                  _F64, _F64, _P]),
     "ukan_kan_backward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),

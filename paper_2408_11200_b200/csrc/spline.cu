@@ -504,6 +504,29 @@ bool kan_bwd_dmma_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, boo
 int kan_bwd_dmma_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
                           float* dscale, double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid,
                           const RegPlan& p, cudaStream_t st);
+struct SwPlan {
+  bool ok = false;
+  int rm = 0, ov = 1, Z = 1, sps = 0, d_pad = 0;
+  size_t smem = 0;
+  int64_t g64_bytes = 0, part_bytes = 0;
+};
+SwPlan kan_bwd_sw_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base);
+int64_t kan_bwd_sw_workspace(const SwPlan& p);
+template <int K>
+int kan_bwd_sw_run(const float* x, const float* gy, const float* C, const float* scale, float* dC, float* dscale,
+                   float* dbw, void* ws, int B, int d_in, int d_out, int R, const KanGrid& grid, const SwPlan& p,
+                   cudaStream_t st);
+struct TmPlan {
+  bool ok = false;
+  int RP = 0, fpc = 0, S = 1, n_ot = 0, Bp = 0;
+  size_t smem = 0;
+  int64_t pack_bytes = 0, rec_bytes = 0, part_bytes = 0;
+};
+TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
+int64_t kan_fwd_tm_workspace(const TmPlan& p);
+template <int K>
+int kan_fwd_tm_run(const float* x, const float* C, const float* scale, float* y, void* ws, int64_t ws_bytes, int B,
+                   int d_in, int d_out, int R, const KanGrid& grid, const TmPlan& p, int32_t* err, cudaStream_t st);
 template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
@@ -614,10 +637,24 @@ static int check_kan_args(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int
 
 using namespace ukan;
 
-extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float* scale,
-                                const float* base_weight, float* y, int64_t B, int64_t d_in,
-                                int64_t d_out, int64_t G, int k, double g_min, double g_max,
-                                int32_t* err_flag, void* stream) {
+// Forward kernel choice: the TMEM-gather kernel (kan_fwd_tm.cu) whenever its plan applies
+// (no base branch, K <= 8, (G-1+window)*OV <= 256); the shared-memory gather otherwise.
+// UKAN_FWD=smem selects the latter for A/B measurement.
+static bool fwd_use_tm() {
+  static const char* e = getenv("UKAN_FWD");
+  return e == nullptr || e[0] != 's';
+}
+
+extern "C" int64_t ukan_kan_forward_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k) {
+  if (k < 0 || k > UKAN_MAX_DEGREE || G < 1 || B < 0 || d_in < 1 || d_out < 1) return 0;
+  return fwd_use_tm() ? kan_fwd_tm_workspace(kan_fwd_tm_plan(B, d_in, d_out, G, k, false)) : 0;
+}
+
+extern "C" int ukan_kan_forward_ws(const float* x, const float* coeffs, const float* scale,
+                                   const float* base_weight, float* y, int64_t B, int64_t d_in,
+                                   int64_t d_out, int64_t G, int k, double g_min, double g_max,
+                                   int32_t* err_flag, void* workspace, int64_t workspace_bytes,
+                                   void* stream) {
   int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
   if (rc) return rc;
   if (!coeffs || !scale || (B > 0 && (!x || !y))) return UKAN_E_ARG;
@@ -626,8 +663,29 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
   rm.grid = make_kan_grid(g_min, g_max, G);
   rm.R = (int)(G + k);
   cudaStream_t st = (cudaStream_t)stream;
+  if (base_weight == nullptr && fwd_use_tm()) {
+    const TmPlan tp = kan_fwd_tm_plan(B, d_in, d_out, G, k, false);
+    if (tp.ok) {
+      if (workspace == nullptr || workspace_bytes < kan_fwd_tm_workspace(tp)) return UKAN_E_WORKSPACE;
+      UKAN_DISPATCH_K(k, return kan_fwd_tm_run<K>(x, coeffs, scale, y, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out, rm.R, rm.grid, tp, err_flag, st););
+    }
+  }
   UKAN_DISPATCH_K(k, return launch_fwd<K, false>(x, coeffs, scale, base_weight, y, (int)B, (int)d_in, (int)d_out, rm, err_flag, st););
   return UKAN_OK;
+}
+
+extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float* scale,
+                                const float* base_weight, float* y, int64_t B, int64_t d_in,
+                                int64_t d_out, int64_t G, int k, double g_min, double g_max,
+                                int32_t* err_flag, void* stream) {
+  // Convenience entry without a caller workspace: a stream-ordered allocation (no host sync).
+  const int64_t nbytes = base_weight ? 0 : ukan_kan_forward_workspace_size(B, d_in, d_out, G, k);
+  void* ws = nullptr;
+  if (nbytes > 0) UKAN_CUDA_TRY(cudaMallocAsync(&ws, (size_t)nbytes, (cudaStream_t)stream));
+  const int rc = ukan_kan_forward_ws(x, coeffs, scale, base_weight, y, B, d_in, d_out, G, k, g_min, g_max,
+                                     err_flag, ws, nbytes, stream);
+  if (ws) cudaFreeAsync(ws, (cudaStream_t)stream);
+  return rc;
 }
 
 extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
@@ -637,7 +695,8 @@ extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int
   const bool dm = kan_bwd_dmma_plan(B, d_in, d_out, (int)(G + k), k + 1, false, kan_num_sms(), dp);
   const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, (int)(G + k), k + 1, true, kan_num_sms());
   const int64_t tc = kan_bwd_tc_workspace(kan_bwd_tc_plan(B, d_in, d_out, G, k, false));
-  if (p.ok) return std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc);
+  const int64_t sw = kan_bwd_sw_workspace(kan_bwd_sw_plan(B, d_in, d_out, (int)(G + k), k + 1, true));
+  if (p.ok) return std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc), sw);
   if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
 }
@@ -647,8 +706,32 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
                              const float* gy, float* dx, float* dC, float* dscale, float* dbw, void* workspace,
                              int64_t workspace_bytes, int B, int d_in, int d_out, const RowMap& rm,
                              cudaStream_t st) {
-  static const bool no_tc = getenv("UKAN_NO_TC") != nullptr;
-  if (!no_tc && K == 4 && bw == nullptr && B > 0) {  // FP64 tensor-core path (kan_bwd_tc.cu)
+  // UKAN_BWD selects the table-gradient kernel for A/B measurement ("tc" default: banded DMMA,
+  // kan_bwd_tc.cu; "sw": register accumulators, kan_bwd_sw.cu; "dmma", "reg": older variants).
+  static const char* sel_env = getenv("UKAN_BWD");
+  const char* sel = sel_env ? sel_env : "tc";
+  bool table_done = false;
+  if (sel[0] == 's' && B > 0) {
+    const SwPlan sp = kan_bwd_sw_plan(B, d_in, d_out, rm.R, K, bw != nullptr);
+    if (sp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_sw_workspace(sp)) {
+      int rc = kan_bwd_sw_run<K>(x, gy, coeffs, scale, dC, dscale, dbw, workspace, B, d_in, d_out, rm.R, rm.grid,
+                                 sp, st);
+      if (rc) return rc;
+      table_done = true;
+    }
+  }
+  if (table_done) {
+    if (dx) {
+      if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+      const Basis<K> bas = make_basis<K>(K - 1);
+      const int64_t pairs = (int64_t)B * d_in;
+      spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
+                                                                             d_out, rm, bas);
+      UKAN_LAUNCH_CHECK();
+    }
+    return UKAN_OK;
+  }
+  if (sel[0] == 't' && K == 4 && bw == nullptr && B > 0) {  // FP64 tensor-core path (kan_bwd_tc.cu)
     const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, rm.R - K + 1, K - 1, false);
     if (tp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_tc_workspace(tp)) {
       int rc = kan_bwd_tc_run(x, coeffs, scale, gy, dC, dscale, workspace, workspace_bytes, B, d_in, d_out,
@@ -666,8 +749,7 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
     }
   }
   RegPlan p;
-  static const bool no_dmma = getenv("UKAN_NO_DMMA") != nullptr;
-  const bool dm = !no_dmma && kan_bwd_dmma_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms(), p);
+  const bool dm = sel[0] == 'd' && kan_bwd_dmma_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms(), p);
   if (!dm) p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms());
   if (!p.ok)
     return launch_bwd<K, false>(x, coeffs, scale, bw, gy, dx, dC, dscale, dbw, (double*)workspace, B, d_in, d_out,

@@ -72,8 +72,11 @@ class KanSplineFn(torch.autograd.Function):
         d_out = coeffs.shape[2]
         y = torch.empty((B, d_out), device=x.device, dtype=torch.float32)
         err = torch.zeros(1, device=x.device, dtype=torch.int32)
-        check(lib.ukan_kan_forward(ptr(x), ptr(coeffs), ptr(scale), ptr(base_weight), ptr(y), B, d_in,
-                                   d_out, G, k, g_min, g_max, ptr(err), stream_ptr()), "kan_forward")
+        nbytes = 0 if base_weight is not None else lib.ukan_kan_forward_workspace_size(B, d_in, d_out, G, k)
+        ws = torch.empty(nbytes, device=x.device, dtype=torch.uint8) if nbytes > 0 else None
+        check(lib.ukan_kan_forward_ws(ptr(x), ptr(coeffs), ptr(scale), ptr(base_weight), ptr(y), B, d_in,
+                                      d_out, G, k, g_min, g_max, ptr(err), ptr(ws), nbytes, stream_ptr()),
+              "kan_forward")
         _nan_check(err)
         ctx.save_for_backward(x, coeffs, scale, base_weight)
         ctx.meta = (G, k, float(g_min), float(g_max))

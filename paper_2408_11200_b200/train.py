@@ -135,10 +135,13 @@ class SplineTrainer:
         y = torch.empty((B, layer.d_out), device=self.device, dtype=torch.float32)
         if isinstance(layer, KanLayer):
           with self._mark(f"layer{self._li}.kan_forward"):
-            check(self.lib.ukan_kan_forward(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(layer.base_weight),
-                                            ptr(y), B, layer.d_in, layer.d_out, layer.G, layer.k,
-                                            float(layer.g_min), float(layer.g_max), ptr(self._err), st),
-                  "kan_forward")
+            nbytes = 0 if layer.base_weight is not None else self.lib.ukan_kan_forward_workspace_size(
+                B, layer.d_in, layer.d_out, layer.G, layer.k)
+            ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8) if nbytes > 0 else None
+            check(self.lib.ukan_kan_forward_ws(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(layer.base_weight),
+                                               ptr(y), B, layer.d_in, layer.d_out, layer.G, layer.k,
+                                               float(layer.g_min), float(layer.g_max), ptr(self._err), ptr(ws),
+                                               nbytes, st), "kan_forward")
             self.kernel_launches += 1
             return y, None
         keys = ops.ukan_build_keys(h, layer.k, float(layer.delta_g))

@@ -34,9 +34,12 @@ def main():
     ws = torch.empty(max(nb, 8), device=dev, dtype=torch.uint8)
     flush = torch.empty(64 << 20, device=dev, dtype=torch.float32)
 
+    nf = lib.ukan_kan_forward_workspace_size(B, d_in, d_out, G, k)
+    wsf = torch.empty(max(nf, 8), device=dev, dtype=torch.uint8)
+
     def fwd():
-        assert lib.ukan_kan_forward(ptr(x), ptr(C), ptr(sc), None, ptr(y), B, d_in, d_out, G, k, -1.0, 1.0,
-                                    ptr(err), stream_ptr()) == 0
+        assert lib.ukan_kan_forward_ws(ptr(x), ptr(C), ptr(sc), None, ptr(y), B, d_in, d_out, G, k, -1.0, 1.0,
+                                       ptr(err), ptr(wsf), nf, stream_ptr()) == 0
 
     def bwd():
         assert lib.ukan_kan_backward_ws(ptr(x), ptr(C), ptr(sc), None, ptr(gy), ptr(dx), ptr(dC), ptr(ds), None,
