@@ -206,7 +206,7 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
   constexpr int KP = (K + 3) / 4 * 4;
   constexpr int LO = kTmOT / OV;  // 64 output slots
   constexpr int NWARP = kTmThreads / 32;
-  static_assert(2 * kTmWarpsQ * SW == kTmST, "tile shape");
+  static_assert(2 * kTmWarpsQ * SW == kTmST && SW % 4 == 0, "tile shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t full_s[kTmSDepth], empty_s[kTmSDepth];
@@ -298,21 +298,32 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     const float* wr = reinterpret_cast<const float*>(bp + slab_bytes) + (size_t)sb * KP;
     const uint8_t* cr = bp + slab_bytes + recw_bytes + sb;
     const uint32_t tcol = tl + (uint32_t)((g & 1) * RP * OV);
+    // two samples per TMEM wait; the cells of four samples come in one 32-bit load
 #pragma unroll
-    for (int s = 0; s < SW; ++s) {
-      float c[NW];
-      tm_ld<NW>(tcol + (uint32_t)cr[s] * OV, c);
-      float w[KP];
+    for (int s = 0; s < SW; s += 4) {
+      const uint32_t c4 = *reinterpret_cast<const uint32_t*>(cr + s);
 #pragma unroll
-      for (int j = 0; j < KP; j += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(wr + (size_t)s * KP + j);
-        w[j] = a.x; w[j + 1] = a.y; w[j + 2] = a.z; w[j + 3] = a.w;
+      for (int h = 0; h < 4; h += 2) {
+        float c0[NW], c1[NW];
+        tm_ld<NW>(tcol + ((c4 >> (8 * h)) & 0xffu) * OV, c0);
+        tm_ld<NW>(tcol + ((c4 >> (8 * h + 8)) & 0xffu) * OV, c1);
+        float w0[KP], w1[KP];
+#pragma unroll
+        for (int j = 0; j < KP; j += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(wr + (size_t)(s + h) * KP + j);
+          const float4 b = *reinterpret_cast<const float4*>(wr + (size_t)(s + h + 1) * KP + j);
+          w0[j] = a.x; w0[j + 1] = a.y; w0[j + 2] = a.z; w0[j + 3] = a.w;
+          w1[j] = b.x; w1[j + 1] = b.y; w1[j + 2] = b.z; w1[j + 3] = b.w;
+        }
+        tm_wait_ld();
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+#pragma unroll
+          for (int v = 0; v < OV; ++v) {
+            acc[s + h][v] = fmaf(w0[j], c0[j * OV + v], acc[s + h][v]);
+            acc[s + h + 1][v] = fmaf(w1[j], c1[j * OV + v], acc[s + h + 1][v]);
+          }
       }
-      tm_wait_ld();  // 4 warps per scheduler cover the TMEM load latency
-#pragma unroll
-      for (int j = 0; j < K; ++j)
-#pragma unroll
-        for (int v = 0; v < OV; ++v) acc[s][v] = fmaf(w[j], c[j * OV + v], acc[s][v]);
     }
     __syncwarp();
     if (lane == 0)  // done with stage g's shared buffer (slab copied into TMEM, records read)
