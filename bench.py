@@ -210,7 +210,8 @@ def our_arm(args, rank, world, local_rank):
 
     # ---- device-timed region (inputs resident in HBM) ----
     tr.timers = {}
-    launches0 = tr.kernel_launches
+    lib = P._lib.load()
+    launches0 = lib.ukan_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
@@ -221,7 +222,7 @@ def our_arm(args, rank, world, local_rank):
         end.record()
         torch.cuda.synchronize()
         barrier()
-    launches = (tr.kernel_launches - launches0) // max(1, args.steps)
+    launches = (lib.ukan_launch_count() - launches0) // max(1, args.steps)
     ms = start.elapsed_time(end)
     tr.read_loss(loss)
     ops.flush_checks()
@@ -267,13 +268,15 @@ def our_arm(args, rank, world, local_rank):
     fwd_ms = kern_ms.get("layer0.kan_forward")
     bwd_ms = kern_ms.get("layer0.kan_backward")
     if bwd_ms and fwd_ms and bwd_ms >= fwd_ms:
-        dom, dom_ms, dom_fl, dom_peak, bound = "spline_bwd_table_kernel (layer0)", bwd_ms, f_bwd, FP64_TFLOPS_MEASURED, "fp64-fma"
+        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 backward: kan_bwd_tc_prep + kan_bwd_tc_sweep (FP64 DMMA)", bwd_ms,
+                                                f_bwd, FP64_TFLOPS_MEASURED, "fp64-fma")
     else:
-        dom, dom_ms, dom_fl, dom_peak, bound = "spline_fwd_kernel (layer0)", fwd_ms, f_fwd, FP32_TFLOPS_MEASURED, "fp32-fma"
+        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 forward: kan_pack + kan_fwd_records + kan_fwd_tm (TMEM gather)",
+                                                fwd_ms, f_fwd, FP32_TFLOPS_MEASURED, "fp32-fma")
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     # compulsory HBM bytes of the dominant launch
     R = CFG["G"] + k
-    if dom.startswith("spline_bwd"):
+    if "backward" in dom:
         hbm_bytes = 4.0 * (B * d0 + B * d1 + 2 * d0 * R * d1 + 3 * d0 * d1)
     else:
         hbm_bytes = 4.0 * (B * d0 + B * d1 + d0 * R * d1 + d0 * d1)

@@ -39,6 +39,10 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch). */
 int ukan_version(void);
 
+/* Number of kernels this library has launched in the process so far (monotonic; for
+ * benchmarks and tests that check the native path actually ran). */
+int64_t ukan_launch_count(void);
+
 /* Exact K x K basis matrix (K = k+1) of the uniform degree-k B-spline in monomial form,
  * row i = coefficient of u^i, column j = window slot j; computed by the Cox-de Boor recursion
  * in exact rational arithmetic and rounded once to double.  Replaces

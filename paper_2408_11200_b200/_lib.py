@@ -33,6 +33,7 @@ _F32 = ctypes.c_float
 # name -> (restype, argtypes); mirrors include/ukan_b200.h one to one
 SIGNATURES: dict[str, tuple] = {
     "ukan_version": (_INT, []),
+    "ukan_launch_count": (_I64, []),
     "ukan_basis_matrix": (_INT, [_INT, _P]),
     "ukan_kan_forward": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _P]),
     "ukan_kan_forward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),

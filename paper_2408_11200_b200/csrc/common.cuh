@@ -16,7 +16,14 @@
     if (_e != cudaSuccess) return (int)_e;                      \
   } while (0)
 
-#define UKAN_LAUNCH_CHECK() UKAN_CUDA_TRY(cudaGetLastError())
+// Every kernel launch of the library is followed by UKAN_LAUNCH_CHECK(), which also counts it
+// (ukan_launch_count(), for the benchmark's gpu_launches figure).
+extern "C" void ukan_note_launch(void);
+#define UKAN_LAUNCH_CHECK()  \
+  do {                       \
+    ukan_note_launch();      \
+    UKAN_CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 namespace ukan {
 

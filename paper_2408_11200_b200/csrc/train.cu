@@ -1,3 +1,4 @@
+#include <atomic>
 // train.cu — training-step kernels: losses and the optimizer update.
 //
 // Replaces tensor.mse / softmax_cross_entropy (tensor.py:368-400), optim.adam_step
@@ -147,5 +148,9 @@ extern "C" int ukan_fill_f32(float* p, int64_t n, float value, void* stream) {
 }
 
 extern "C" int ukan_version(void) { return 100; }
+
+static std::atomic<int64_t> g_launches{0};
+extern "C" void ukan_note_launch(void) { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" int64_t ukan_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int ukan_basis_matrix(int k, double* M_out) { return ukan_basis_matrix_impl(k, M_out); }
