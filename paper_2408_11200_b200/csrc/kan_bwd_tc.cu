@@ -23,6 +23,7 @@
 // products and sums throughout.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -273,6 +274,149 @@ kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __r
   }
 }
 
+// Two warps per feature ("tc2"): warp h of feature f owns blocks [h*RB/2, (h+1)*RB/2), so a
+// warp holds half the block accumulators and can cover twice the outputs (NT = 8 DMMA tiles
+// per group share one A operand).  The two halves meet in a shared-memory fp64 row buffer in
+// fixed order (block order, half 0 before half 1) -> deterministic.
+template <int RB, int NT>
+__global__ void __launch_bounds__(256, 1)
+kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
+                         const float* __restrict__ scale, const float* __restrict__ gy,
+                         float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
+                         int B, int d_in, int d_out, int G, int nch, int cps, Basis<4> bas) {
+  constexpr int OPB = 8 * NT;
+  constexpr int FPB = 4;
+  constexpr int BH = RB / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  const int fl = warp >> 1, h = warp & 1;
+  const int i0 = blockIdx.x * FPB;
+  const int i = i0 + fl;
+  const int o0 = blockIdx.y * OPB;
+  const int z = blockIdx.z;
+  const int n_lo = z * cps, n_hi = min(nch, n_lo + cps);
+  const int R = G + 3;
+  const size_t rb = tc_rec_bytes(G);
+  __shared__ double Msh[16];
+  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  unsigned char* rec_s = smem_raw;                                              // 2 x [FPB][rb]
+  float* g_s = reinterpret_cast<float*>(smem_raw + 2 * FPB * rb);               // 2 x [BC][OPB]
+
+  auto stage = [&](int n, int buf) {
+    unsigned char* dst = rec_s + (size_t)buf * FPB * rb;
+    const int q = (int)(rb / 16);
+    for (int t = threadIdx.x; t < FPB * q; t += blockDim.x) {
+      const int f = t / q, c = t % q;
+      const bool ok = i0 + f < d_in;
+      const unsigned char* src = ok ? recs + ((size_t)(i0 + f) * nch + n) * rb + (size_t)c * 16 : recs;
+      tc_cp16(dst + (size_t)f * rb + (size_t)c * 16, src, ok ? 16 : 0);
+    }
+    float* gd = g_s + (size_t)buf * kTcBC * OPB;
+    const int b0 = n * kTcBC;
+    const int nb = min(kTcBC, B - b0);
+    if ((d_out & 3) == 0) {
+      constexpr int q4 = OPB / 4;
+      for (int t = threadIdx.x; t < kTcBC * q4; t += blockDim.x) {
+        const int s = t / q4, oc = (t % q4) * 4;
+        const int o = o0 + oc;
+        const int bytes = (s < nb) ? max(0, min(4, d_out - o)) * 4 : 0;
+        tc_cp16(gd + s * OPB + oc, bytes ? gy + (size_t)(b0 + s) * d_out + o : gy, bytes);
+      }
+    } else {
+      for (int t = threadIdx.x; t < kTcBC * OPB; t += blockDim.x) {
+        const int s = t / OPB, oc = t % OPB;
+        const bool ok = s < nb && o0 + oc < d_out;
+        tc_cp4(gd + t, ok ? gy + (size_t)(b0 + s) * d_out + o0 + oc : gy, ok);
+      }
+    }
+  };
+
+  double acc[BH][NT][2];
+#pragma unroll
+  for (int bb = 0; bb < BH; ++bb)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[bb][t][0] = acc[bb][t][1] = 0.0;
+
+  if (n_lo < n_hi) stage(n_lo, 0);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int n = n_lo; n < n_hi; ++n) {
+    const int buf = (n - n_lo) & 1;
+    if (n + 1 < n_hi) stage(n + 1, buf ^ 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    if (i < d_in) {
+      const unsigned char* rec = rec_s + ((size_t)buf * FPB + fl) * rb;
+      const int* ent = reinterpret_cast<const int*>(rec);
+      const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
+      const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
+      const float* gl = g_s + (size_t)buf * kTcBC * OPB + grp;
+#pragma unroll
+      for (int bl = 0; bl < BH; ++bl) {
+        const int bb = h * BH + bl;
+        const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
+#pragma unroll 2
+        for (int kc = e0; kc < e1; kc += 4) {
+          const int pos = kc + kq;
+          const bool vld = pos < e1;
+          const int e = ent[min(pos, kTcBC - 1)];
+          const double u = uu[min(pos, kTcBC - 1)];
+          const int j = grp - ((e >> 8) & 3);
+          double a = 0.0;
+          if (vld && j >= 0 && j < 4) a = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+          const int srow = (e & 255) * OPB;
+          double bf[NT];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) bf[t] = vld ? (double)gl[srow + t * 8] : 0.0;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) tc_dmma(acc[bl][t][0], acc[bl][t][1], a, bf[t]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // epilogue: rows of both halves meet in S[FPB][R][OPB] (fp64, reuses the staging space)
+  double* S = reinterpret_cast<double*>(smem_raw);
+  const int RR = 4 * RB + 4;
+  for (int t = threadIdx.x; t < FPB * RR * OPB; t += blockDim.x) S[t] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    if (h == hh) {
+#pragma unroll
+      for (int bl = 0; bl < BH; ++bl) {
+        const int r = 4 * (h * BH + bl) + grp;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) S[((size_t)fl * RR + r) * OPB + t * 8 + 2 * kq + v] += acc[bl][t][v];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < FPB * OPB; t += blockDim.x) {
+    const int f = t / OPB, oc = t % OPB;
+    const int ii = i0 + f, o = o0 + oc;
+    if (ii >= d_in || o >= d_out) continue;
+    const double* Sf = S + (size_t)f * RR * OPB + oc;
+    if (part != nullptr) {
+      for (int r = 0; r < R; ++r) part[(size_t)z * d_in * R * d_out + ((size_t)ii * R + r) * d_out + o] = Sf[(size_t)r * OPB];
+    } else {
+      const double sc = (double)scale[(size_t)ii * d_out + o];
+      double ds = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const size_t ci = ((size_t)ii * R + r) * d_out + o;
+        const double a = Sf[(size_t)r * OPB];
+        dC[ci] = (float)(sc * a);
+        ds = fma((double)C[ci], a, ds);
+      }
+      dscale[(size_t)ii * d_out + o] = (float)ds;
+    }
+  }
+}
+
 __global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const float* __restrict__ C,
                                          const float* __restrict__ scale, float* __restrict__ dC,
                                          float* __restrict__ dscale, int S, int d_in, int d_out, int R) {
@@ -296,6 +440,7 @@ __global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const 
 struct TcPlan {
   bool ok = false;
   int rb = 0, nt = 4, S = 1, cps = 0, nch = 0;
+  bool split = false;
   size_t smem = 0;
   int64_t rec_bytes = 0, part_bytes = 0;
 };
@@ -316,12 +461,17 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   const int rbn = (int)((G - 1) >> 2) + 1;
   p.rb = rbn <= 4 ? 4 : (rbn <= 8 ? 8 : 16);
   p.nt = p.rb == 16 ? 2 : (d_out <= 8 ? 1 : (d_out <= 16 ? 2 : 4));
+  static const bool no_tc2 = getenv("UKAN_NO_TC2") != nullptr;  // A/B measurement only
+  p.split = !no_tc2 && p.rb >= 8 && d_out >= 32;  // two warps per feature (tc2 kernel)
+  if (p.split) p.nt = (p.rb == 8 && d_out >= 64) ? 8 : 4;
   const int opb = 8 * p.nt;
+  const int fpb = p.split ? 4 : 8;
   p.nch = (int)((B + kTcBC - 1) / kTcBC);
-  p.smem = 2 * 8 * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * opb;
+  p.smem = 2 * fpb * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * opb;
+  if (p.split) p.smem = std::max<size_t>(p.smem, sizeof(double) * (size_t)fpb * (4 * p.rb + 4) * opb);
   p.rec_bytes = (int64_t)d_in * p.nch * (int64_t)tc_rec_bytes((int)G);
   const int sms = tc_sms();
-  const int64_t base = ((d_in + 7) / 8) * ((d_out + opb - 1) / opb);
+  const int64_t base = ((d_in + fpb - 1) / fpb) * ((d_out + opb - 1) / opb);
   int64_t S = 1;
   if (base < 2 * (int64_t)sms) {
     const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(16, p.nch / 4));
@@ -340,6 +490,25 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
 }
 
 int64_t kan_bwd_tc_workspace(const TcPlan& p) { return p.ok ? ((p.rec_bytes + 255) / 256) * 256 + p.part_bytes : 0; }
+
+template <int RB, int NT>
+static int tc2_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                      unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
+                      cudaStream_t st) {
+  auto kern = kan_bwd_tc2_sweep_kernel<RB, NT>;
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  dim3 gridd((d_in + 3) / 4, (d_out + 8 * NT - 1) / (8 * NT), p.S);
+  kern<<<gridd, 256, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
+                                   p.nch, p.cps, make_basis<4>(3));
+  UKAN_LAUNCH_CHECK();
+  if (p.S > 1) {
+    const int64_t n = (int64_t)d_in * d_out;
+    kan_bwd_tc_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, C, scale, dC, dscale, p.S, d_in,
+                                                                          d_out, G + 3);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
 
 template <int RB, int NT>
 static int tc_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
@@ -369,6 +538,9 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
   dim3 pg((d_in + 7) / 8, p.nch);
   kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid);
   UKAN_LAUNCH_CHECK();
+  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8) return tc2_launch<8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16) return tc2_launch<16, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4) return tc_launch<4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
