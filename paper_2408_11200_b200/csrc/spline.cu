@@ -529,6 +529,12 @@ template <int K>
 int kan_fwd_tm_run(const float* x, const float* C, const float* scale, float* y, void* ws, int64_t ws_bytes, int B,
                    int d_in, int d_out, int R, const KanGrid& grid, const TmPlan& p, int32_t* err, cudaStream_t st);
 template <int K>
+int kan_fwd_narrow(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
+                   int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
+template <int K>
+int kan_dx_narrow2(const float* x, const float* C, const float* scale, const float* bw, const float* gy, float* dx,
+                   int B, int d_in, int d_out, int R, const KanGrid& grid, cudaStream_t st);
+template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
 
@@ -638,8 +644,9 @@ static int check_kan_args(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int
 
 using namespace ukan;
 
-// Forward kernel choice: the TMEM-gather kernel (kan_fwd_tm.cu) whenever its plan applies
-// (no base branch, K <= 8, (G-1+window)*OV <= 256); the shared-memory gather otherwise.
+// Forward kernel choice: d_out <= 32 -> lanes-over-samples kernel (kan_narrow.cu); else the
+// TMEM-gather kernel (kan_fwd_tm.cu) whenever its plan applies (no base branch, K <= 8,
+// G <= 255, (G-1+window)*4 <= 256); the shared-memory gather otherwise.
 // UKAN_FWD=smem selects the latter for A/B measurement.
 static bool fwd_use_tm() {
   static const char* e = getenv("UKAN_FWD");
@@ -664,6 +671,9 @@ extern "C" int ukan_kan_forward_ws(const float* x, const float* coeffs, const fl
   rm.grid = make_kan_grid(g_min, g_max, G);
   rm.R = (int)(G + k);
   cudaStream_t st = (cudaStream_t)stream;
+  if (d_out <= 32 && fwd_use_tm()) {  // narrow layer: lanes over samples (kan_narrow.cu)
+    UKAN_DISPATCH_K(k, return kan_fwd_narrow<K>(x, coeffs, scale, base_weight, y, (int)B, (int)d_in, (int)d_out, rm.R, rm.grid, err_flag, st););
+  }
   if (base_weight == nullptr && fwd_use_tm()) {
     const TmPlan tp = kan_fwd_tm_plan(B, d_in, d_out, G, k, false);
     if (tp.ok) {
@@ -723,7 +733,7 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
   }
   if (table_done) {
     if (dx) {
-      if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+      if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
       const Basis<K> bas = make_basis<K>(K - 1);
       const int64_t pairs = (int64_t)B * d_in;
       spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
@@ -739,7 +749,7 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
                               rm.R - K + 1, rm.grid, tp, st);
       if (rc) return rc;
       if (dx) {
-        if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+        if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
         const Basis<K> bas = make_basis<K>(K - 1);
         const int64_t pairs = (int64_t)B * d_in;
         spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
@@ -765,7 +775,7 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
                                         rm.R, rm.grid, p, st);
   if (rc) return rc;
   if (dx && B > 0) {
-    if (d_out <= 32) return kan_dx_narrow<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+    if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
     const Basis<K> bas = make_basis<K>(K - 1);
     const int64_t pairs = (int64_t)B * d_in;
     const int wpb = 8;
