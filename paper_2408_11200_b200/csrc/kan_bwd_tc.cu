@@ -278,14 +278,13 @@ kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __r
 // warp holds half the block accumulators and can cover twice the outputs (NT = 8 DMMA tiles
 // per group share one A operand).  The two halves meet in a shared-memory fp64 row buffer in
 // fixed order (block order, half 0 before half 1) -> deterministic.
-template <int RB, int NT>
-__global__ void __launch_bounds__(256, 1)
+template <int RB, int NT, int FPB>
+__global__ void __launch_bounds__(FPB * 64, 1)
 kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
                          const float* __restrict__ scale, const float* __restrict__ gy,
                          float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
                          int B, int d_in, int d_out, int G, int nch, int cps, Basis<4> bas) {
   constexpr int OPB = 8 * NT;
-  constexpr int FPB = 4;
   constexpr int BH = RB / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -302,6 +301,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
   unsigned char* rec_s = smem_raw;                                              // 2 x [FPB][rb]
   float* g_s = reinterpret_cast<float*>(smem_raw + 2 * FPB * rb);               // 2 x [BC][OPB]
+  double* w_s = reinterpret_cast<double*>(g_s + (size_t)2 * kTcBC * OPB);       // [FPB][BC][4] basis weights
 
   auto stage = [&](int n, int buf) {
     unsigned char* dst = rec_s + (size_t)buf * FPB * rb;
@@ -346,10 +346,19 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
+    // basis weights of the chunk's sorted samples, once per CTA (fp64 Horner, layers.py:29-37)
+    for (int t = threadIdx.x; t < FPB * kTcBC; t += blockDim.x) {
+      const int f = t / kTcBC, pos = t % kTcBC;
+      const double u = reinterpret_cast<const double*>(rec_s + ((size_t)buf * FPB + f) * rb + kTcBC * 4)[pos];
+      double* wd = w_s + (size_t)t * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wd[j] = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+    }
+    __syncthreads();
     if (i < d_in) {
       const unsigned char* rec = rec_s + ((size_t)buf * FPB + fl) * rb;
+      const double* wf = w_s + (size_t)fl * kTcBC * 4;
       const int* ent = reinterpret_cast<const int*>(rec);
-      const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
       const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
       const float* gl = g_s + (size_t)buf * kTcBC * OPB + grp;
 #pragma unroll
@@ -360,15 +369,15 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
         for (int kc = e0; kc < e1; kc += 4) {
           const int pos = kc + kq;
           const bool vld = pos < e1;
-          const int e = ent[min(pos, kTcBC - 1)];
-          const double u = uu[min(pos, kTcBC - 1)];
+          const int pc = min(pos, kTcBC - 1);
+          const int e = ent[pc];
           const int j = grp - ((e >> 8) & 3);
-          double a = 0.0;
-          if (vld && j >= 0 && j < 4) a = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+          const double wj = wf[pc * 4 + (j & 3)];
+          const double a = (vld && j >= 0 && j < 4) ? wj : 0.0;
           const int srow = (e & 255) * OPB;
-          double bf[NT];
+          double bf[NT];  // rows of invalid positions are real (zero-filled) samples: a = 0 masks them
 #pragma unroll
-          for (int t = 0; t < NT; ++t) bf[t] = vld ? (double)gl[srow + t * 8] : 0.0;
+          for (int t = 0; t < NT; ++t) bf[t] = (double)gl[srow + t * 8];
 #pragma unroll
           for (int t = 0; t < NT; ++t) tc_dmma(acc[bl][t][0], acc[bl][t][1], a, bf[t]);
         }
@@ -439,7 +448,7 @@ __global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const 
 // ---------------------------------------------------------------------------------------
 struct TcPlan {
   bool ok = false;
-  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0;
+  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0, fpb = 4;
   bool split = false;
   size_t smem = 0;
   int64_t rec_bytes = 0, part_bytes = 0;
@@ -463,12 +472,19 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   p.nt = p.rb == 16 ? 2 : (d_out <= 8 ? 1 : (d_out <= 16 ? 2 : 4));
   static const bool no_tc2 = getenv("UKAN_NO_TC2") != nullptr;  // A/B measurement only
   p.split = !no_tc2 && p.rb >= 8 && d_out >= 32;  // two warps per feature (tc2 kernel)
-  if (p.split) p.nt = (p.rb == 8 && d_out >= 64) ? 8 : 4;
+  // 16 warps x NT=4 (default) measured 1.88 ms vs 8 warps x NT=8 1.94 ms on KAN 784->256, B=8192;
+  // UKAN_TC2_NT=8 selects the latter (A/B measurement only)
+  static const int tc2_wide = getenv("UKAN_TC2_NT") ? atoi(getenv("UKAN_TC2_NT")) : 4;
+  if (p.split) p.nt = (p.rb == 8 && d_out >= 64 && tc2_wide == 8) ? 8 : 4;
+  if (p.split && p.rb == 8 && p.nt == 4 && tc2_wide == 4) p.fpb = 8;  // 16 warps, 8 features
   const int opb = 8 * p.nt;
-  const int fpb = p.split ? 4 : 8;
+  const int fpb = p.split ? p.fpb : 8;
   p.nch = (int)((B + kTcBC - 1) / kTcBC);
   p.smem = 2 * fpb * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * opb;
-  if (p.split) p.smem = std::max<size_t>(p.smem, sizeof(double) * (size_t)fpb * (4 * p.rb + 4) * opb);
+  if (p.split) {
+    p.smem += sizeof(double) * (size_t)fpb * kTcBC * 4;  // per-sample basis weights
+    p.smem = std::max<size_t>(p.smem, sizeof(double) * (size_t)fpb * (4 * p.rb + 4) * opb);
+  }
   p.rec_bytes = (int64_t)d_in * p.nch * (int64_t)tc_rec_bytes((int)G);
   const int sms = tc_sms();
   const int64_t base = ((d_in + fpb - 1) / fpb) * ((d_out + opb - 1) / opb);
@@ -491,14 +507,14 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
 
 int64_t kan_bwd_tc_workspace(const TcPlan& p) { return p.ok ? ((p.rec_bytes + 255) / 256) * 256 + p.part_bytes : 0; }
 
-template <int RB, int NT>
+template <int RB, int NT, int FPB>
 static int tc2_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                       unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
                       cudaStream_t st) {
-  auto kern = kan_bwd_tc2_sweep_kernel<RB, NT>;
+  auto kern = kan_bwd_tc2_sweep_kernel<RB, NT, FPB>;
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  dim3 gridd((d_in + 3) / 4, (d_out + 8 * NT - 1) / (8 * NT), p.S);
-  kern<<<gridd, 256, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
+  dim3 gridd((d_in + FPB - 1) / FPB, (d_out + 8 * NT - 1) / (8 * NT), p.S);
+  kern<<<gridd, FPB * 64, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
                                    p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
@@ -538,9 +554,10 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
   dim3 pg((d_in + 7) / 8, p.nch);
   kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid);
   UKAN_LAUNCH_CHECK();
-  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8) return tc2_launch<8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 16) return tc2_launch<16, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8) return tc2_launch<8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16) return tc2_launch<16, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4) return tc_launch<4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
