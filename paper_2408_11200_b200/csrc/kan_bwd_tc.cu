@@ -274,22 +274,24 @@ kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __r
   }
 }
 
-// Two warps per feature ("tc2"): warp h of feature f owns blocks [h*RB/2, (h+1)*RB/2), so a
-// warp holds half the block accumulators and can cover twice the outputs (NT = 8 DMMA tiles
-// per group share one A operand).  The two halves meet in a shared-memory fp64 row buffer in
-// fixed order (block order, half 0 before half 1) -> deterministic.
-template <int RB, int NT, int FPB>
-__global__ void __launch_bounds__(FPB * 64, 1)
+// WPF warps per feature ("tc2"): warp h of feature f owns blocks [h*RB/WPF, (h+1)*RB/WPF), so a
+// warp holds a fraction of the block accumulators and can cover more outputs (NT DMMA tiles per
+// group share one A operand).  The parts meet in a shared-memory fp64 row buffer in fixed order
+// (block order, part 0 first) -> deterministic.
+template <int RB, int NT, int FPB, int WPF>
+__global__ void __launch_bounds__(FPB * WPF * 32, 1)
 kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
                          const float* __restrict__ scale, const float* __restrict__ gy,
                          float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
                          int B, int d_in, int d_out, int G, int nch, int cps, Basis<4> bas) {
   constexpr int OPB = 8 * NT;
-  constexpr int BH = RB / 2;
+  constexpr int GST = OPB + 8;  // g row stride (floats): +32 B puts the 4 sample rows of a DMMA
+                                // B operand on disjoint banks (one wavefront instead of four)
+  constexpr int BH = RB / WPF;  // blocks per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, kq = lane & 3;
-  const int fl = warp >> 1, h = warp & 1;
+  const int fl = warp / WPF, h = warp % WPF;
   const int i0 = blockIdx.x * FPB;
   const int i = i0 + fl;
   const int o0 = blockIdx.y * OPB;
@@ -301,7 +303,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
   unsigned char* rec_s = smem_raw;                                              // 2 x [FPB][rb]
   float* g_s = reinterpret_cast<float*>(smem_raw + 2 * FPB * rb);               // 2 x [BC][OPB]
-  double* w_s = reinterpret_cast<double*>(g_s + (size_t)2 * kTcBC * OPB);       // [FPB][BC][4] basis weights
+  double* w_s = reinterpret_cast<double*>(g_s + (size_t)2 * kTcBC * GST);       // [FPB][BC][4] basis weights
 
   auto stage = [&](int n, int buf) {
     unsigned char* dst = rec_s + (size_t)buf * FPB * rb;
@@ -312,7 +314,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
       const unsigned char* src = ok ? recs + ((size_t)(i0 + f) * nch + n) * rb + (size_t)c * 16 : recs;
       tc_cp16(dst + (size_t)f * rb + (size_t)c * 16, src, ok ? 16 : 0);
     }
-    float* gd = g_s + (size_t)buf * kTcBC * OPB;
+    float* gd = g_s + (size_t)buf * kTcBC * GST;
     const int b0 = n * kTcBC;
     const int nb = min(kTcBC, B - b0);
     if ((d_out & 3) == 0) {
@@ -321,13 +323,13 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
         const int s = t / q4, oc = (t % q4) * 4;
         const int o = o0 + oc;
         const int bytes = (s < nb) ? max(0, min(4, d_out - o)) * 4 : 0;
-        tc_cp16(gd + s * OPB + oc, bytes ? gy + (size_t)(b0 + s) * d_out + o : gy, bytes);
+        tc_cp16(gd + s * GST + oc, bytes ? gy + (size_t)(b0 + s) * d_out + o : gy, bytes);
       }
     } else {
       for (int t = threadIdx.x; t < kTcBC * OPB; t += blockDim.x) {
         const int s = t / OPB, oc = t % OPB;
         const bool ok = s < nb && o0 + oc < d_out;
-        tc_cp4(gd + t, ok ? gy + (size_t)(b0 + s) * d_out + o0 + oc : gy, ok);
+        tc_cp4(gd + s * GST + oc, ok ? gy + (size_t)(b0 + s) * d_out + o0 + oc : gy, ok);
       }
     }
   };
@@ -360,7 +362,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
       const double* wf = w_s + (size_t)fl * kTcBC * 4;
       const int* ent = reinterpret_cast<const int*>(rec);
       const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
-      const float* gl = g_s + (size_t)buf * kTcBC * OPB + grp;
+      const float* gl = g_s + (size_t)buf * kTcBC * GST + grp;
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
         const int bb = h * BH + bl;
@@ -374,7 +376,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
           const int j = grp - ((e >> 8) & 3);
           const double wj = wf[pc * 4 + (j & 3)];
           const double a = (vld && j >= 0 && j < 4) ? wj : 0.0;
-          const int srow = (e & 255) * OPB;
+          const int srow = (e & 255) * GST;
           double bf[NT];  // rows of invalid positions are real (zero-filled) samples: a = 0 masks them
 #pragma unroll
           for (int t = 0; t < NT; ++t) bf[t] = (double)gl[srow + t * 8];
@@ -391,7 +393,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   for (int t = threadIdx.x; t < FPB * RR * OPB; t += blockDim.x) S[t] = 0.0;
   __syncthreads();
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
+  for (int hh = 0; hh < WPF; ++hh) {
     if (h == hh) {
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
@@ -448,7 +450,7 @@ __global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const 
 // ---------------------------------------------------------------------------------------
 struct TcPlan {
   bool ok = false;
-  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0, fpb = 4;
+  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0, fpb = 4, wpf = 2;
   bool split = false;
   size_t smem = 0;
   int64_t rec_bytes = 0, part_bytes = 0;
@@ -472,15 +474,20 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   p.nt = p.rb == 16 ? 2 : (d_out <= 8 ? 1 : (d_out <= 16 ? 2 : 4));
   static const bool no_tc2 = getenv("UKAN_NO_TC2") != nullptr;  // A/B measurement only
   p.split = !no_tc2 && p.rb >= 8 && d_out >= 32;  // two warps per feature (tc2 kernel)
-  // 16 warps x NT=4 (default) measured 1.88 ms vs 8 warps x NT=8 1.94 ms on KAN 784->256, B=8192;
-  // UKAN_TC2_NT=8 selects the latter (A/B measurement only)
-  static const int tc2_wide = getenv("UKAN_TC2_NT") ? atoi(getenv("UKAN_TC2_NT")) : 4;
+  // Layer 0 of cfg2 (KAN 784->256, B=8192): 4 warps per feature x NT=8 ("16", default) 1.74 ms;
+  // 2 warps x NT=4 with 8 features ("4") 1.88 ms; 2 warps x NT=8 ("8") 1.94 ms (A/B via UKAN_TC2_NT)
+  static const int tc2_wide = getenv("UKAN_TC2_NT") ? atoi(getenv("UKAN_TC2_NT")) : 16;
   if (p.split) p.nt = (p.rb == 8 && d_out >= 64 && tc2_wide == 8) ? 8 : 4;
   if (p.split && p.rb == 8 && p.nt == 4 && tc2_wide == 4) p.fpb = 8;  // 16 warps, 8 features
+  if (p.split && p.rb == 8 && d_out >= 64 && tc2_wide == 16) {  // 16 warps: 4 features x 4 block parts, NT = 8
+    p.wpf = 4;
+    p.nt = 8;
+    p.fpb = 4;
+  }
   const int opb = 8 * p.nt;
   const int fpb = p.split ? p.fpb : 8;
   p.nch = (int)((B + kTcBC - 1) / kTcBC);
-  p.smem = 2 * fpb * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * opb;
+  p.smem = 2 * fpb * tc_rec_bytes((int)G) + sizeof(float) * (size_t)2 * kTcBC * (opb + (p.split ? 8 : 0));
   if (p.split) {
     p.smem += sizeof(double) * (size_t)fpb * kTcBC * 4;  // per-sample basis weights
     p.smem = std::max<size_t>(p.smem, sizeof(double) * (size_t)fpb * (4 * p.rb + 4) * opb);
@@ -507,14 +514,14 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
 
 int64_t kan_bwd_tc_workspace(const TcPlan& p) { return p.ok ? ((p.rec_bytes + 255) / 256) * 256 + p.part_bytes : 0; }
 
-template <int RB, int NT, int FPB>
+template <int RB, int NT, int FPB, int WPF>
 static int tc2_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                       unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
                       cudaStream_t st) {
-  auto kern = kan_bwd_tc2_sweep_kernel<RB, NT, FPB>;
+  auto kern = kan_bwd_tc2_sweep_kernel<RB, NT, FPB, WPF>;
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 gridd((d_in + FPB - 1) / FPB, (d_out + 8 * NT - 1) / (8 * NT), p.S);
-  kern<<<gridd, FPB * 64, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
+  kern<<<gridd, FPB * WPF * 32, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
                                    p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
@@ -554,10 +561,11 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
   dim3 pg((d_in + 7) / 8, p.nch);
   kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid);
   UKAN_LAUNCH_CHECK();
-  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8) return tc2_launch<8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 16) return tc2_launch<16, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.wpf == 4) return tc2_launch<8, 8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16) return tc2_launch<16, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4) return tc_launch<4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);

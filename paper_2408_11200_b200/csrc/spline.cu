@@ -491,7 +491,7 @@ int kan_dx_narrow(const float* x, const float* C, const float* scale, const floa
 int kan_num_sms();
 struct TcPlan {
   bool ok = false;
-  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0, fpb = 4;
+  int rb = 0, nt = 4, S = 1, cps = 0, nch = 0, fpb = 4, wpf = 2;
   bool split = false;
   size_t smem = 0;
   int64_t rec_bytes = 0, part_bytes = 0;
