@@ -29,7 +29,7 @@
 
 namespace ukan {
 
-constexpr int kTcBC = 128;  // samples per chunk
+constexpr int kTcBC = 256;  // samples per chunk (the sample index is packed in 8 bits)
 
 // prep record layout (bytes, 16-aligned): ent[128] int | u[128] double | st[NBP] int
 __host__ __device__ constexpr int tc_nbp(int G) { return ((G + 1 + 3) / 4) * 4; }
