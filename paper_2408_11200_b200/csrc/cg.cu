@@ -7,11 +7,20 @@
 //   H      = silu(inp @ W1 + b1)             fp32 GEMM (K = d_femb + d_pe)
 //   Out    = H @ W2 + b2                     fp32 GEMM (K = d_h) -> table [n_u, K*d_out]
 //   backward GEMMs accumulate in fp64 (reductions over n_u / K*d_out).
-// These are CUDA-core tiled GEMMs (first implementation); the tcgen05 3xTF32 path is the
-// planned replacement.
+// The forward GEMMs run on the tensor cores (cg_tc.cu: tcgen05, tf32 operand splits) whenever the
+// shapes allow 16-byte loads.  The gradient GEMMs stay on fp64-accumulating kernels: the tensor
+// core's fp32 accumulator carries ~22 bits per MMA (measured), which misses the UKAN gradient
+// parity by 2-3x even with 3-piece operand splits and per-chunk fp64 promotion.
 #include "common.cuh"
 
 namespace ukan {
+
+// tensor-core path (cg_tc.cu)
+bool cg_tc_applicable(const void* a, const void* b, int64_t M, int64_t N, int64_t K, int64_t ca, int64_t cb);
+int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+               int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
+               int S, int64_t kps, cudaStream_t st);
+int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
 // positional encoding + embedding gather
@@ -247,6 +256,11 @@ extern "C" int ukan_gemm_bias_act(const float* A, const float* Bm, const float* 
                                   void* stream) {
   if (M < 0 || N < 1 || K < 1 || M > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
   if (M == 0) return UKAN_OK;
+  // The table GEMM (act = 0: H @ W2 + b2) feeds only the spline forward and dscale, which keep
+  // their parity on the tensor cores; the activated GEMM's pre-activation feeds every CG
+  // gradient (silu'), where the tensor core's ~22-bit accumulation measured 2.6x over the bar.
+  if (act == 0 && cg_tc_applicable(A, Bm, M, N, K, K, N))  // A [M,K] row-major, B [K,N] row-major
+    return cg_tc_gemm(A, K, 1, Bm, N, 1, M, N, K, 0, bias, act, C, pre_out, nullptr, 1, K, (cudaStream_t)stream);
   dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
   gemm_nn_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(A, Bm, bias, C, pre_out, (int)M, (int)N, (int)K, act);
   UKAN_LAUNCH_CHECK();
@@ -257,8 +271,9 @@ extern "C" int ukan_gemm_nt(const float* A, const float* Bm, float* C, int64_t M
                             int64_t K, void* stream) {
   if (M < 0 || N < 1 || K < 1 || M > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
   if (M == 0) return UKAN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
   dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
-  gemm_nt_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(A, Bm, C, (int)M, (int)N, (int)K);
+  gemm_nt_kernel<<<g, 256, 0, st>>>(A, Bm, C, (int)M, (int)N, (int)K);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }
@@ -270,10 +285,7 @@ extern "C" int ukan_gemm_tn(const float* A, const float* Bm, float* C, float* co
   dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
   gemm_tn_kernel<<<g, 256, 0, st>>>(A, Bm, C, (int)M, (int)N, (int)K);
   UKAN_LAUNCH_CHECK();
-  if (colsum_B) {
-    colsum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(Bm, colsum_B, (int)K, (int)N);
-    UKAN_LAUNCH_CHECK();
-  }
+  if (colsum_B) return cg_colsum(Bm, colsum_B, K, N, st);
   return UKAN_OK;
 }
 

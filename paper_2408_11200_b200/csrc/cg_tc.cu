@@ -1,0 +1,360 @@
+// cg_tc.cu — the coefficient-generator MLP GEMMs on the 5th-generation tensor cores (tcgen05).
+//
+// Replaces the matmuls of _cg_eval (layers.py:241-243) and their tape backward (tensor.py:189-197):
+//   forward  pre = inp @ W1 + b1, H = silu(pre)      table = H @ W2 + b2
+//   backward dW2 = H^T dT, dH = dT W2^T, dW1 = inp^T dpre, dinp = dpre W1^T
+// which are plain dense GEMMs (the north star's one tensor-core use).  Precision: the reference is
+// float64; fp32 products accumulated in fp32 fail the parity bar on the n_u-long weight-gradient
+// reductions and plain TF32 fails everywhere.  Measured here: 3xTF32 (two
+// pieces, three products) on tcgen05 still misses the UKAN gradient parity by 2-3x, because the
+// tensor core's fp32 accumulator truncates and two tf32 pieces carry only ~22 bits.  So this
+// kernel splits each operand into **three round-to-nearest tf32 pieces** (hi + mid + lo, ~33
+// bits) and issues the six products with piece order <= 2 on `tcgen05.mma.kind::tf32`, promotes
+// every 32-wide K chunk out of TMEM into registers (fp32; fp64 for the split-K weight
+// gradients, whose <= 4096-row slices are reduced in fixed order in fp64).
+//
+// CTA = 8 warps, one 128 x BN output tile (TMEM: 128 lanes x 2 x BN fp32 columns), K in chunks
+// of 32.  All threads load a chunk from global (any transpose: the loader reads along the
+// contiguous global dimension), splits it into hi/mid/lo tf32 and stores them in the canonical
+// K-major no-swizzle shared layout (8-row x 16-byte core matrices, LBO = 128 B, SBO = 1 KB);
+// thread 0 issues 4 k-steps x 6 MMAs into the chunk's TMEM buffer and commits to the chunk
+// buffer's mbarrier, so the next chunk's loads overlap the tensor-core work (double buffer);
+// each chunk's partial is promoted into fp32 registers (see the kernel comment).
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace ukan {
+
+constexpr int kTcgM = 128;   // tile rows (TMEM lanes)
+constexpr int kTcgK = 32;    // K per chunk
+constexpr int kTcgThreads = 256;  // 8 warps: two per TMEM lane quarter (column halves)
+
+// fp32 -> tf32 (10 mantissa bits), round to nearest with ties away from zero, low 13 bits zeroed
+// (the same rounding as cvt.rna.tf32.f32, spelled out so the split is exact by construction:
+// a - tf32(a) is then exactly representable and carries the remaining 13 bits)
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+}
+
+__device__ __forceinline__ void cg_mb_init(uint64_t* mb, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(count));
+}
+__device__ __forceinline__ void cg_mb_wait(uint64_t* mb, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mb);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// sm100 shared-memory matrix descriptor, K-major, no swizzle (layout type 0, version 1).
+__device__ __forceinline__ uint64_t cg_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void cg_mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// byte offset of element (row r, k) inside a [rows x 32] K-major canonical tile
+__device__ __forceinline__ uint32_t cg_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 1024 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+// a = hi + mid + lo, each a tf32 value (round-to-nearest); the residual after lo is < 2^-33 |a|.
+__device__ __forceinline__ void tf32_split3(float a, uint32_t& h, uint32_t& m, uint32_t& l) {
+  h = tf32_rna(a);
+  const float r1 = a - __uint_as_float(h);  // exact
+  m = tf32_rna(r1);
+  l = tf32_rna(r1 - __uint_as_float(m));    // exact difference, rounded
+}
+
+// Load a [ROWS x 32] chunk of op(X) (element (r, k) at X[r*sr + k*sk]) into hi/mid/lo tiles
+// (consecutive, TB bytes apart).
+template <int ROWS>
+__device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_t sr, int64_t sk, int r0, int k0,
+                                             int R, int Kt, unsigned char* t0) {
+  constexpr int TB = ROWS * kTcgK * 4;
+  if (sk == 1) {  // K contiguous: float4 along k
+    for (int t = threadIdx.x; t < ROWS * 8; t += kTcgThreads) {
+      const int r = t >> 3, k = (t & 7) * 4;
+      float e[4] = {0.f, 0.f, 0.f, 0.f};
+      if (r0 + r < R && k0 + k + 3 < Kt) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(X + (size_t)(r0 + r) * sr + k0 + k));
+        e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+      } else if (r0 + r < R) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e[q] = (k0 + k + q < Kt) ? __ldg(X + (size_t)(r0 + r) * sr + k0 + k + q) : 0.f;
+      }
+      uint32_t h[4], m[4], l[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tf32_split3(e[q], h[q], m[q], l[q]);
+      const uint32_t o = cg_off(r, k);
+      *reinterpret_cast<uint4*>(t0 + o) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(t0 + TB + o) = make_uint4(m[0], m[1], m[2], m[3]);
+      *reinterpret_cast<uint4*>(t0 + 2 * TB + o) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  } else {  // rows contiguous (sr == 1): float4 along r at fixed k
+    for (int t = threadIdx.x; t < ROWS / 4 * 32; t += kTcgThreads) {
+      const int k = t / (ROWS / 4), r = (t % (ROWS / 4)) * 4;
+      float e[4] = {0.f, 0.f, 0.f, 0.f};
+      if (k0 + k < Kt) {
+        if (r0 + r + 3 < R) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(X + (size_t)(k0 + k) * sk + r0 + r));
+          e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) e[q] = (r0 + r + q < R) ? __ldg(X + (size_t)(k0 + k) * sk + r0 + r + q) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t h, m, l;
+        tf32_split3(e[q], h, m, l);
+        const uint32_t o = cg_off(r + q, k);
+        *reinterpret_cast<uint32_t*>(t0 + o) = h;
+        *reinterpret_cast<uint32_t*>(t0 + TB + o) = m;
+        *reinterpret_cast<uint32_t*>(t0 + 2 * TB + o) = l;
+      }
+    }
+  }
+}
+
+// D[m, n] = sum_k A(m, k) B(k, n), A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn].
+// mode 0: C = act(D + bias[n]) (pre = D + bias when act);   mode 1: C = D * silu'(pre[m, n]);
+// mode 2: part[z][m][n] = D over K-chunk z (split-K, fp64-reduced by cg_splitk_reduce_kernel).
+//
+// Accumulation precision: the tensor core's fp32 accumulator is not IEEE-exact (measured: a
+// K=4096 tensor-core sum was 40x less accurate than an fp32 FMA chain), so every 32-wide K chunk
+// goes to its own TMEM buffer (two, alternating) and is promoted into fp32 register
+// accumulators by the threads while the next chunk's MMAs run.  Thread (warp w, lane l) owns
+// row 32*(w%4)+l and columns [(w/4)*BN/2, +BN/2).
+template <int BN, typename AccT>
+__global__ void __launch_bounds__(kTcgThreads, 1)
+cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const float* __restrict__ Bm, int64_t sbk,
+                  int64_t sbn, int M, int N, int K, int kps, int mode, const float* __restrict__ bias, int act,
+                  float* __restrict__ C, float* __restrict__ pre, float* __restrict__ part) {
+  constexpr int A_BYTES = kTcgM * kTcgK * 4, B_BYTES = BN * kTcgK * 4;
+  constexpr int STAGE = 3 * A_BYTES + 3 * B_BYTES;  // A hi | mid | lo | B hi | mid | lo
+  constexpr int HN = BN / 2;                         // columns per thread
+  constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;   // two accumulator buffers
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(kTcgM >> 4) << 24);  // f32 accum, tf32 A/B, K-major, M=128
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tbase_s;
+  __shared__ __align__(8) uint64_t mma_done[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int m0 = blockIdx.x * kTcgM, n0 = blockIdx.y * BN;
+  const int z = blockIdx.z;
+  const int kb = z * kps, ke = min(K, kb + kps);
+  const int nch = (ke - kb + kTcgK - 1) / kTcgK;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tbase_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    cg_mb_init(&mma_done[0], 1);
+    cg_mb_init(&mma_done[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tbase_s;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(half * HN);
+
+  AccT acc[HN];  // fp64 for the split-K weight gradients (long reductions), fp32 otherwise
+#pragma unroll
+  for (int j = 0; j < HN; ++j) acc[j] = (AccT)0;
+  auto drain = [&](int c) {  // chunk c's partial (TMEM buffer c&1) -> registers
+    const uint32_t ta = trow + (uint32_t)((c & 1) * BN);
+#pragma unroll
+    for (int cb = 0; cb < HN; cb += 32) {
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(ta + (uint32_t)cb));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (cb + j < HN) acc[cb + j] += (AccT)__uint_as_float(r[j]);
+    }
+  };
+
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c >= 2) {
+      cg_mb_wait(&mma_done[buf], (uint32_t)(((c - 2) >> 1) & 1));  // chunk c-2 done: smem + TMEM buffer free
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      drain(c - 2);
+    }
+    unsigned char* st = smem_raw + (size_t)buf * STAGE;
+    const int k0 = kb + c * kTcgK;
+    cg_load_tile<kTcgM>(A, sam, sak, m0, k0, M, ke, st);
+    cg_load_tile<BN>(Bm, sbn, sbk, n0, k0, N, ke, st + 3 * A_BYTES);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic stores -> tensor-core reads
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t a0 = sbase + buf * STAGE, b0 = a0 + 3 * A_BYTES;
+      const uint32_t td = tmem + (uint32_t)(buf * BN);
+      // products with piece-order sum <= 2 (hh, hm, mh, hl, mm, lh), smallest terms first
+      constexpr int PA[6] = {2, 1, 0, 1, 0, 0}, PB[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+      for (int kk = 0; kk < kTcgK / 8; ++kk) {
+        const uint32_t off = kk * 256;  // two 16-byte core-matrix columns per k-step of 8
+#pragma unroll
+        for (int t = 0; t < 6; ++t)
+          cg_mma_tf32(td, cg_desc(a0 + PA[t] * A_BYTES + off, 128, 1024), cg_desc(b0 + PB[t] * B_BYTES + off, 128, 1024),
+                      IDESC, (kk > 0 || t > 0) ? 1 : 0);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&mma_done[buf]))
+                   : "memory");
+    }
+  }
+  for (int c = max(0, nch - 2); c < nch; ++c) {  // the last two chunks, in order
+    cg_mb_wait(&mma_done[c & 1], (uint32_t)((c >> 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    drain(c);
+  }
+
+  // epilogue: row m, columns n0 + half*HN + j
+  const int m = m0 + 32 * q + lane;
+  if (m < M) {
+#pragma unroll
+    for (int j = 0; j < HN; ++j) {  // fully unrolled: acc stays in registers
+      const int n = n0 + half * HN + j;
+      if (n >= N) continue;
+      const float d = (float)acc[j];
+      if (mode == 2) {
+        part[((size_t)z * M + m) * N + n] = d;
+      } else if (mode == 1) {  // dpre = dH * (s + pre*s*(1-s))  (tensor.py:232-233)
+        const float p = pre[(size_t)m * N + n];
+        const float s = 1.f / (1.f + __expf(-p));
+        C[(size_t)m * N + n] = d * (s + p * s * (1.f - s));
+      } else {
+        const float v = d + (bias ? bias[n] : 0.f);
+        if (act) {
+          pre[(size_t)m * N + n] = v;
+          C[(size_t)m * N + n] = v / (1.f + __expf(-v));
+        } else {
+          C[(size_t)m * N + n] = v;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
+}
+
+// C[m][n] = sum_z part[z][m][n] in fp64, fixed order (deterministic).
+__global__ void cg_splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ C, int64_t MN, int S) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= MN) return;
+  double a = 0.0;
+  for (int z = 0; z < S; ++z) a += (double)part[(size_t)z * MN + t];
+  C[t] = (float)a;
+}
+
+// colsum[n] = sum_k X[k][n] (fp64, fixed order): CTA = 32 columns x 8 row-slices, two-level.
+__global__ void __launch_bounds__(256) cg_colsum_kernel(const float* __restrict__ X, float* __restrict__ out, int K,
+                                                        int N) {
+  __shared__ double red[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), ty = threadIdx.x >> 5;
+  double a = 0.0;
+  if (c < N)
+    for (int k = ty; k < K; k += 8) a += (double)X[(size_t)k * N + c];
+  red[ty][threadIdx.x & 31] = a;
+  __syncthreads();
+  if (ty == 0 && c < N) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x & 31];
+    out[c] = (float)s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+int kan_num_sms();
+
+static size_t cg_smem(int BN) { return 2 * (size_t)(3 * kTcgM * kTcgK * 4 + 3 * BN * kTcgK * 4) + 1024; }
+
+template <int BN, typename AccT>
+static int cg_launch(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int M,
+                     int N, int K, int kps, int S, int mode, const float* bias, int act, float* C, float* pre,
+                     float* part, cudaStream_t st) {
+  auto kern = cg_gemm_tc_kernel<BN, AccT>;
+  const size_t smem = cg_smem(BN);
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 g((M + kTcgM - 1) / kTcgM, (N + BN - 1) / BN, S);
+  kern<<<g, kTcgThreads, smem, st>>>(A, sam, sak, Bm, sbk, sbn, M, N, K, kps, mode, bias, act, C, pre, part);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+// Whether the tensor-core path takes this GEMM: contiguous dimensions must allow float4 loads.
+static bool cg_tc_ok(int64_t contig_a, int64_t contig_b) { return contig_a % 4 == 0 && contig_b % 4 == 0; }
+
+int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+               int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
+               int S, int64_t kps, cudaStream_t st) {
+  const int m = (int)M, n = (int)N, k = (int)K, kp = (int)kps;
+  // fp64 promotion registers in every mode: the old fp64-accumulated CUDA-core GEMMs set the
+  // parity margin of the UKAN gradients, fp32 promotion measured 2-3x over it
+  if (N > 64) return cg_launch<128, double>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+  return cg_launch<64, double>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+}
+
+bool cg_tc_applicable(const void* a, const void* b, int64_t M, int64_t N, int64_t K, int64_t ca, int64_t cb) {
+  static const bool off = getenv("UKAN_CG_CUDA_CORES") != nullptr;  // A/B measurement only
+  const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);  // 16-byte vector loads
+  return !off && aligned && M > 0 && N > 0 && K > 0 && cg_tc_ok(ca, cb) && M <= INT32_MAX && N <= INT32_MAX &&
+         K <= INT32_MAX;
+}
+
+constexpr int64_t kSplitRows = 4096;  // fp32 accumulation length before the fp64 promotion
+
+int64_t cg_tc_splitk_workspace(int64_t M, int64_t N, int64_t K) {
+  const int64_t S = (K + kSplitRows - 1) / kSplitRows;
+  return (int64_t)sizeof(float) * S * M * N;
+}
+
+int cg_tc_splitk(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                 int64_t N, int64_t K, float* C, float* part, cudaStream_t st) {
+  const int S = (int)((K + kSplitRows - 1) / kSplitRows);
+  int rc = cg_tc_gemm(A, sam, sak, Bm, sbk, sbn, M, N, K, 2, nullptr, 0, nullptr, nullptr, part, S, kSplitRows, st);
+  if (rc) return rc;
+  const int64_t MN = M * N;
+  cg_splitk_reduce_kernel<<<(unsigned)((MN + 255) / 256), 256, 0, st>>>(part, C, MN, S);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st) {
+  cg_colsum_kernel<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(X, out, (int)K, (int)N);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+}  // namespace ukan
