@@ -7,10 +7,12 @@
 //   H      = silu(inp @ W1 + b1)             fp32 GEMM (K = d_femb + d_pe)
 //   Out    = H @ W2 + b2                     fp32 GEMM (K = d_h) -> table [n_u, K*d_out]
 //   backward GEMMs accumulate in fp64 (reductions over n_u / K*d_out).
-// The forward GEMMs run on the tensor cores (cg_tc.cu: tcgen05, tf32 operand splits) whenever the
-// shapes allow 16-byte loads.  The gradient GEMMs stay on fp64-accumulating kernels: the tensor
-// core's fp32 accumulator carries ~22 bits per MMA (measured), which misses the UKAN gradient
-// parity by 2-3x even with 3-piece operand splits and per-chunk fp64 promotion.
+// Tensor cores for every GEMM: the table GEMM on tcgen05 (cg_tc.cu, tf32 operand splits); the
+// gradient GEMMs on the FP64 tensor cores (cg_dmma.cu, IEEE fp64 products and sums) because the
+// tcgen05 fp32 accumulator carries ~22 bits per MMA (measured), which misses the UKAN gradient
+// parity by 2-3x even with 3-piece operand splits and per-chunk fp64 promotion.  The
+// activated GEMM (its pre-activation feeds every gradient) and misaligned shapes use the fp32
+// CUDA-core kernel below.
 #include "common.cuh"
 
 namespace ukan {
@@ -21,6 +23,19 @@ int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_
                int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
                int S, int64_t kps, cudaStream_t st);
 int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st);
+// fp64 tensor-core gradient GEMMs (cg_dmma.cu)
+int64_t cg_dmma_workspace(int64_t M, int64_t N, int64_t K);
+int cg_dmma_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                 int64_t N, int64_t K, float* C, double* part, cudaStream_t st);
+static int dmma_with_ws(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                        int64_t N, int64_t K, float* C, cudaStream_t st) {
+  const int64_t nb = cg_dmma_workspace(M, N, K);
+  void* part = nullptr;  // split-K partials: stream-ordered allocation, no host sync
+  if (nb > 0) UKAN_CUDA_TRY(cudaMallocAsync(&part, (size_t)nb, st));
+  const int rc = cg_dmma_gemm(A, sam, sak, Bm, sbk, sbn, M, N, K, C, static_cast<double*>(part), st);
+  if (part) cudaFreeAsync(part, st);
+  return rc;
+}
 
 // ---------------------------------------------------------------------------------------
 // positional encoding + embedding gather
@@ -108,110 +123,8 @@ gemm_nn_kernel(const float* __restrict__ A, const float* __restrict__ Bm,
   }
 }
 
-// C[M,N] = A[M,K] @ B[N,K]^T, fp64 accumulate.
-__global__ void __launch_bounds__(256)
-gemm_nt_kernel(const float* __restrict__ A, const float* __restrict__ Bm, float* __restrict__ C,
-               int M, int N, int K) {
-  __shared__ float As[TK][TM + 4];
-  __shared__ float Bs[TK][TN + 4];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += TK) {
-    for (int t = threadIdx.x; t < TM * TK; t += 256) {
-      const int mm = t / TK, kk = t % TK;
-      const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < K) ? A[(size_t)gm * K + gk] : 0.f;
-    }
-    for (int t = threadIdx.x; t < TN * TK; t += 256) {
-      const int nn = t / TK, kk = t % TK;
-      const int gn = n0 + nn, gk = k0 + kk;
-      Bs[kk][nn] = (gn < N && gk < K) ? Bm[(size_t)gn * K + gk] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = (double)As[kk][ty * 4 + q];
-        b[q] = (double)Bs[kk][tx * 4 + q];
-      }
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int gm = m0 + ty * 4 + p;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int gn = n0 + tx * 4 + q;
-      if (gn < N) C[(size_t)gm * N + gn] = (float)acc[p][q];
-    }
-  }
-}
 
-// C[M,N] = A[K,M]^T @ B[K,N], fp64 accumulate over the (long) K = n_u dimension.
-__global__ void __launch_bounds__(256)
-gemm_tn_kernel(const float* __restrict__ A, const float* __restrict__ Bm, float* __restrict__ C,
-               int M, int N, int K) {
-  __shared__ float As[TK][TM + 4];
-  __shared__ float Bs[TK][TN + 4];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += TK) {
-    for (int t = threadIdx.x; t < TK * TM; t += 256) {
-      const int kk = t / TM, mm = t % TM;
-      const int gk = k0 + kk, gm = m0 + mm;
-      As[kk][mm] = (gk < K && gm < M) ? A[(size_t)gk * M + gm] : 0.f;
-    }
-    for (int t = threadIdx.x; t < TK * TN; t += 256) {
-      const int kk = t / TN, nn = t % TN;
-      const int gk = k0 + kk, gn = n0 + nn;
-      Bs[kk][nn] = (gk < K && gn < N) ? Bm[(size_t)gk * N + gn] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = (double)As[kk][ty * 4 + q];
-        b[q] = (double)Bs[kk][tx * 4 + q];
-      }
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int gm = m0 + ty * 4 + p;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int gn = n0 + tx * 4 + q;
-      if (gn < N) C[(size_t)gm * N + gn] = (float)acc[p][q];
-    }
-  }
-}
 
-// colsum[n] = sum_k B[k, n] in fp64 (bias gradients), fixed order.
-__global__ void colsum_kernel(const float* __restrict__ Bm, float* __restrict__ out, int K, int N) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  double s = 0.0;
-  for (int k = 0; k < K; ++k) s += (double)Bm[(size_t)k * N + n];
-  out[n] = (float)s;
-}
 
 __global__ void silu_bwd_kernel(const float* __restrict__ pre, const float* __restrict__ dH,
                                 float* __restrict__ dpre, int64_t n) {
@@ -271,22 +184,21 @@ extern "C" int ukan_gemm_nt(const float* A, const float* Bm, float* C, int64_t M
                             int64_t K, void* stream) {
   if (M < 0 || N < 1 || K < 1 || M > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
   if (M == 0) return UKAN_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
-  gemm_nt_kernel<<<g, 256, 0, st>>>(A, Bm, C, (int)M, (int)N, (int)K);
-  UKAN_LAUNCH_CHECK();
-  return UKAN_OK;
+  return dmma_with_ws(A, K, 1, Bm, 1, K, M, N, K, C, (cudaStream_t)stream);  // A [M,K], B given as [N,K]
 }
 
 extern "C" int ukan_gemm_tn(const float* A, const float* Bm, float* C, float* colsum_B,
                             int64_t M, int64_t N, int64_t K, void* stream) {
   if (M < 1 || N < 1 || K < 0 || K > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 g((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
-  gemm_tn_kernel<<<g, 256, 0, st>>>(A, Bm, C, (int)M, (int)N, (int)K);
-  UKAN_LAUNCH_CHECK();
-  if (colsum_B) return cg_colsum(Bm, colsum_B, K, N, st);
-  return UKAN_OK;
+  if (K == 0) {
+    UKAN_CUDA_TRY(cudaMemsetAsync(C, 0, sizeof(float) * M * N, st));
+    if (colsum_B) UKAN_CUDA_TRY(cudaMemsetAsync(colsum_B, 0, sizeof(float) * N, st));
+    return UKAN_OK;
+  }
+  int rc = dmma_with_ws(A, 1, M, Bm, N, 1, M, N, K, C, st);  // A given as [K,M], B [K,N]
+  if (rc) return rc;
+  return colsum_B ? cg_colsum(Bm, colsum_B, K, N, st) : UKAN_OK;
 }
 
 extern "C" int ukan_silu_backward(const float* pre, const float* dH, float* dpre, int64_t n,
