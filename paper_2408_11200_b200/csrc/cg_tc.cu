@@ -8,10 +8,10 @@
 // reductions and plain TF32 fails everywhere.  Measured here: 3xTF32 (two
 // pieces, three products) on tcgen05 still misses the UKAN gradient parity by 2-3x, because the
 // tensor core's fp32 accumulator truncates and two tf32 pieces carry only ~22 bits.  So this
-// kernel splits each operand into **three round-to-nearest tf32 pieces** (hi + mid + lo, ~33
-// bits) and issues the six products with piece order <= 2 on `tcgen05.mma.kind::tf32`, promotes
-// every 32-wide K chunk out of TMEM into registers (fp32; fp64 for the split-K weight
-// gradients, whose <= 4096-row slices are reduced in fixed order in fp64).
+// kernel is used for the table GEMM only (H @ W2 + b2, whose outputs feed the spline forward):
+// operands split into round-to-nearest tf32 pieces (2 pieces / 3 products; a 3-piece / 6-product
+// variant is templated), every 32-wide K chunk promoted out of TMEM into fp32 registers.  The
+// gradient GEMMs run on the FP64 tensor cores (cg_dmma.cu).
 //
 // CTA = 8 warps, one 128 x BN output tile (TMEM: 128 lanes x 2 x BN fp32 columns), K in chunks
 // of 32.  All threads load a chunk from global (any transpose: the loader reads along the
@@ -78,7 +78,7 @@ __device__ __forceinline__ void tf32_split3(float a, uint32_t& h, uint32_t& m, u
 
 // Load a [ROWS x 32] chunk of op(X) (element (r, k) at X[r*sr + k*sk]) into hi/mid/lo tiles
 // (consecutive, TB bytes apart).
-template <int ROWS>
+template <int ROWS, int PIECES>
 __device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_t sr, int64_t sk, int r0, int k0,
                                              int R, int Kt, unsigned char* t0) {
   constexpr int TB = ROWS * kTcgK * 4;
@@ -98,8 +98,14 @@ __device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_
       for (int q = 0; q < 4; ++q) tf32_split3(e[q], h[q], m[q], l[q]);
       const uint32_t o = cg_off(r, k);
       *reinterpret_cast<uint4*>(t0 + o) = make_uint4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<uint4*>(t0 + TB + o) = make_uint4(m[0], m[1], m[2], m[3]);
-      *reinterpret_cast<uint4*>(t0 + 2 * TB + o) = make_uint4(l[0], l[1], l[2], l[3]);
+      if (PIECES == 2) {  // two pieces: the second carries the whole remainder (rounded)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m[q] = tf32_rna(e[q] - __uint_as_float(h[q]));
+        *reinterpret_cast<uint4*>(t0 + TB + o) = make_uint4(m[0], m[1], m[2], m[3]);
+      } else {
+        *reinterpret_cast<uint4*>(t0 + TB + o) = make_uint4(m[0], m[1], m[2], m[3]);
+        *reinterpret_cast<uint4*>(t0 + 2 * TB + o) = make_uint4(l[0], l[1], l[2], l[3]);
+      }
     }
   } else {  // rows contiguous (sr == 1): float4 along r at fixed k
     for (int t = threadIdx.x; t < ROWS / 4 * 32; t += kTcgThreads) {
@@ -120,8 +126,12 @@ __device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_
         tf32_split3(e[q], h, m, l);
         const uint32_t o = cg_off(r + q, k);
         *reinterpret_cast<uint32_t*>(t0 + o) = h;
-        *reinterpret_cast<uint32_t*>(t0 + TB + o) = m;
-        *reinterpret_cast<uint32_t*>(t0 + 2 * TB + o) = l;
+        if (PIECES == 2) {
+          *reinterpret_cast<uint32_t*>(t0 + TB + o) = tf32_rna(e[q] - __uint_as_float(h));
+        } else {
+          *reinterpret_cast<uint32_t*>(t0 + TB + o) = m;
+          *reinterpret_cast<uint32_t*>(t0 + 2 * TB + o) = l;
+        }
       }
     }
   }
@@ -136,13 +146,13 @@ __device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_
 // goes to its own TMEM buffer (two, alternating) and is promoted into fp32 register
 // accumulators by the threads while the next chunk's MMAs run.  Thread (warp w, lane l) owns
 // row 32*(w%4)+l and columns [(w/4)*BN/2, +BN/2).
-template <int BN, typename AccT>
+template <int BN, typename AccT, int PIECES>
 __global__ void __launch_bounds__(kTcgThreads, 1)
 cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const float* __restrict__ Bm, int64_t sbk,
                   int64_t sbn, int M, int N, int K, int kps, int mode, const float* __restrict__ bias, int act,
                   float* __restrict__ C, float* __restrict__ pre, float* __restrict__ part) {
   constexpr int A_BYTES = kTcgM * kTcgK * 4, B_BYTES = BN * kTcgK * 4;
-  constexpr int STAGE = 3 * A_BYTES + 3 * B_BYTES;  // A hi | mid | lo | B hi | mid | lo
+  constexpr int STAGE = PIECES * (A_BYTES + B_BYTES);  // A pieces | B pieces
   constexpr int HN = BN / 2;                         // columns per thread
   constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;   // two accumulator buffers
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -207,24 +217,28 @@ cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const f
     }
     unsigned char* st = smem_raw + (size_t)buf * STAGE;
     const int k0 = kb + c * kTcgK;
-    cg_load_tile<kTcgM>(A, sam, sak, m0, k0, M, ke, st);
-    cg_load_tile<BN>(Bm, sbn, sbk, n0, k0, N, ke, st + 3 * A_BYTES);
+    cg_load_tile<kTcgM, PIECES>(A, sam, sak, m0, k0, M, ke, st);
+    cg_load_tile<BN, PIECES>(Bm, sbn, sbk, n0, k0, N, ke, st + PIECES * A_BYTES);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic stores -> tensor-core reads
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t a0 = sbase + buf * STAGE, b0 = a0 + 3 * A_BYTES;
+      const uint32_t a0 = sbase + buf * STAGE, b0 = a0 + PIECES * A_BYTES;
       const uint32_t td = tmem + (uint32_t)(buf * BN);
-      // products with piece-order sum <= 2 (hh, hm, mh, hl, mm, lh), smallest terms first
-      constexpr int PA[6] = {2, 1, 0, 1, 0, 0}, PB[6] = {0, 1, 2, 0, 1, 0};
+      // products with piece-order sum <= PIECES-1, smallest terms first:
+      //   2 pieces: (h,l) (l,h) (h,h);   3 pieces: (l,h) (m,m) (h,l) (m,h) (h,m) (h,h)
+      constexpr int NP = PIECES == 2 ? 3 : 6;
+      constexpr int PA3[6] = {2, 1, 0, 1, 0, 0}, PB3[6] = {0, 1, 2, 0, 1, 0};
+      constexpr int PA2[3] = {0, 1, 0}, PB2[3] = {1, 0, 0};
 #pragma unroll
       for (int kk = 0; kk < kTcgK / 8; ++kk) {
         const uint32_t off = kk * 256;  // two 16-byte core-matrix columns per k-step of 8
 #pragma unroll
-        for (int t = 0; t < 6; ++t)
-          cg_mma_tf32(td, cg_desc(a0 + PA[t] * A_BYTES + off, 128, 1024), cg_desc(b0 + PB[t] * B_BYTES + off, 128, 1024),
-                      IDESC, (kk > 0 || t > 0) ? 1 : 0);
+        for (int t = 0; t < NP; ++t)
+          cg_mma_tf32(td, cg_desc(a0 + (PIECES == 2 ? PA2[t] : PA3[t]) * A_BYTES + off, 128, 1024),
+                      cg_desc(b0 + (PIECES == 2 ? PB2[t] : PB3[t]) * B_BYTES + off, 128, 1024), IDESC,
+                      (kk > 0 || t > 0) ? 1 : 0);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(&mma_done[buf]))
@@ -267,30 +281,31 @@ cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const f
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
 }
 
-// C[m][n] = sum_z part[z][m][n] in fp64, fixed order (deterministic).
-__global__ void cg_splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ C, int64_t MN, int S) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= MN) return;
-  double a = 0.0;
-  for (int z = 0; z < S; ++z) a += (double)part[(size_t)z * MN + t];
-  C[t] = (float)a;
-}
-
-// colsum[n] = sum_k X[k][n] (fp64, fixed order): CTA = 32 columns x 8 row-slices, two-level.
-__global__ void __launch_bounds__(256) cg_colsum_kernel(const float* __restrict__ X, float* __restrict__ out, int K,
-                                                        int N) {
+// colsum[n] = sum_k X[k][n] (fp64, fixed order): pass 1 sums 32 columns x one row slice per CTA
+// (8 warps, rows interleaved, then the 8 warp sums in order) into part[slice][n]; pass 2 adds the
+// slices in order.
+__global__ void __launch_bounds__(256) cg_colsum_part_kernel(const float* __restrict__ X, double* __restrict__ part,
+                                                             int K, int N, int rows_per_slice) {
   __shared__ double red[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), ty = threadIdx.x >> 5;
+  const int k0 = blockIdx.y * rows_per_slice, k1 = min(K, k0 + rows_per_slice);
   double a = 0.0;
   if (c < N)
-    for (int k = ty; k < K; k += 8) a += (double)X[(size_t)k * N + c];
+    for (int k = k0 + ty; k < k1; k += 8) a += (double)X[(size_t)k * N + c];
   red[ty][threadIdx.x & 31] = a;
   __syncthreads();
   if (ty == 0 && c < N) {
     double s = 0.0;
     for (int q = 0; q < 8; ++q) s += red[q][threadIdx.x & 31];
-    out[c] = (float)s;
+    part[(size_t)blockIdx.y * N + c] = s;
   }
+}
+__global__ void cg_colsum_final_kernel(const double* __restrict__ part, float* __restrict__ out, int N, int S) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  double s = 0.0;
+  for (int z = 0; z < S; ++z) s += part[(size_t)z * N + c];
+  out[c] = (float)s;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -298,14 +313,14 @@ __global__ void __launch_bounds__(256) cg_colsum_kernel(const float* __restrict_
 // ---------------------------------------------------------------------------------------
 int kan_num_sms();
 
-static size_t cg_smem(int BN) { return 2 * (size_t)(3 * kTcgM * kTcgK * 4 + 3 * BN * kTcgK * 4) + 1024; }
+static size_t cg_smem(int BN, int pieces) { return 2 * (size_t)pieces * (kTcgM * kTcgK * 4 + BN * kTcgK * 4) + 1024; }
 
-template <int BN, typename AccT>
+template <int BN, typename AccT, int PIECES>
 static int cg_launch(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int M,
                      int N, int K, int kps, int S, int mode, const float* bias, int act, float* C, float* pre,
                      float* part, cudaStream_t st) {
-  auto kern = cg_gemm_tc_kernel<BN, AccT>;
-  const size_t smem = cg_smem(BN);
+  auto kern = cg_gemm_tc_kernel<BN, AccT, PIECES>;
+  const size_t smem = cg_smem(BN, PIECES);
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 g((M + kTcgM - 1) / kTcgM, (N + BN - 1) / BN, S);
   kern<<<g, kTcgThreads, smem, st>>>(A, sam, sak, Bm, sbk, sbn, M, N, K, kps, mode, bias, act, C, pre, part);
@@ -320,10 +335,12 @@ int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_
                int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
                int S, int64_t kps, cudaStream_t st) {
   const int m = (int)M, n = (int)N, k = (int)K, kp = (int)kps;
-  // fp64 promotion registers in every mode: the old fp64-accumulated CUDA-core GEMMs set the
-  // parity margin of the UKAN gradients, fp32 promotion measured 2-3x over it
-  if (N > 64) return cg_launch<128, double>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
-  return cg_launch<64, double>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+  // Only the table GEMM (mode 0, act 0) takes this path: its outputs feed the spline forward, where
+  // fp32-level accuracy keeps parity — two tf32 pieces (3 products), fp32 promotion registers.
+  if (N >= 256 && (M + kTcgM - 1) / kTcgM * (N / 256) >= kan_num_sms())
+    return cg_launch<256, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+  if (N > 64) return cg_launch<128, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+  return cg_launch<64, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
 }
 
 bool cg_tc_applicable(const void* a, const void* b, int64_t M, int64_t N, int64_t K, int64_t ca, int64_t cb) {
@@ -333,27 +350,17 @@ bool cg_tc_applicable(const void* a, const void* b, int64_t M, int64_t N, int64_
          K <= INT32_MAX;
 }
 
-constexpr int64_t kSplitRows = 4096;  // fp32 accumulation length before the fp64 promotion
-
-int64_t cg_tc_splitk_workspace(int64_t M, int64_t N, int64_t K) {
-  const int64_t S = (K + kSplitRows - 1) / kSplitRows;
-  return (int64_t)sizeof(float) * S * M * N;
-}
-
-int cg_tc_splitk(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
-                 int64_t N, int64_t K, float* C, float* part, cudaStream_t st) {
-  const int S = (int)((K + kSplitRows - 1) / kSplitRows);
-  int rc = cg_tc_gemm(A, sam, sak, Bm, sbk, sbn, M, N, K, 2, nullptr, 0, nullptr, nullptr, part, S, kSplitRows, st);
-  if (rc) return rc;
-  const int64_t MN = M * N;
-  cg_splitk_reduce_kernel<<<(unsigned)((MN + 255) / 256), 256, 0, st>>>(part, C, MN, S);
-  UKAN_LAUNCH_CHECK();
-  return UKAN_OK;
-}
-
 int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st) {
-  cg_colsum_kernel<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(X, out, (int)K, (int)N);
+  const int64_t cblk = (N + 31) / 32;
+  const int S = (int)std::max<int64_t>(1, std::min<int64_t>((4 * kan_num_sms() + cblk - 1) / cblk, (K + 255) / 256));
+  const int rps = (int)((K + S - 1) / S);
+  void* part = nullptr;
+  UKAN_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * S * N, st));
+  cg_colsum_part_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
   UKAN_LAUNCH_CHECK();
+  cg_colsum_final_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(static_cast<double*>(part), out, (int)N, S);
+  UKAN_LAUNCH_CHECK();
+  cudaFreeAsync(part, st);
   return UKAN_OK;
 }
 
