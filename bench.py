@@ -186,8 +186,9 @@ def our_arm(args, rank, world, local_rank):
     import paper_2408_11200_b200 as P
     from paper_2408_11200_b200 import ops
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % torch.cuda.device_count()  # == local_rank on a full node
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     B = CFG["batch"]
     model = P.build_model("kan", CFG["widths"], CFG["k"], seed=0, device=dev, g_min=CFG["g_min"],
                           g_max=CFG["g_max"], G=CFG["G"])
@@ -213,7 +214,7 @@ def our_arm(args, rank, world, local_rank):
     lib = P._lib.load()
     launches0 = lib.ukan_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         torch.cuda.synchronize()
         barrier()
         start.record()
@@ -257,6 +258,7 @@ def our_arm(args, rank, world, local_rank):
     e2e_s = float(t.item())
     e2e_value = world * B * args.steps / e2e_s
 
+    ukan = ukan_layer_rate(dev) if (world == 1 and not args.no_ukan) else None
     if rank != 0:
         return
     pk = peaks()
@@ -311,8 +313,36 @@ def our_arm(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": B * d0 * 4 + B * 8, "d2h_bytes_per_step": 8 + 4},
         "cpu_baseline": cpu,
+        "ukan_layer": ukan,
     }
     print(json.dumps(line), flush=True)
+
+
+def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
+    """Supplementary UKAN measurement (not the headline): one cfg4-shaped UKAN layer (1024 -> 1024,
+    k=3, delta_g=0.5, d_pe=d_femb=32; x ~ N(0, 20^2)) forward + backward of x and every parameter
+    through the drop-in API (key dedup, CG MLP on the tensor cores, spline kernels), device-timed."""
+    import torch
+    import paper_2408_11200_b200 as P
+    layer = P.init_layer("ukan", 1024, 1024, 3, seed=0, delta_g=0.5, d_pe=32, d_femb=32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    x = (torch.randn((B, 1024), device=dev, generator=g) * 20.0).requires_grad_(True)
+    gy = torch.randn((B, 1024), device=dev, generator=g)
+    params = [x] + list(layer.parameters().values())
+    for _ in range(warmup):
+        torch.autograd.grad(P.ukan_forward(layer, x), params, gy)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        torch.autograd.grad(P.ukan_forward(layer, x), params, gy)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    n_u = P.ops.ukan_build_keys(x.detach(), 3, 0.5).n_u
+    return {"workload": "UKAN layer 1024->1024 k=3 delta_g=0.5 d_pe=d_femb=32, x~N(0,20^2), B=4096 (cfg4-shaped)",
+            "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "n_u": n_u, "steps": steps, "warmup": warmup}
 
 
 def main():
@@ -322,6 +352,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ukan", action="store_true", help="skip the supplementary UKAN layer measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -332,8 +363,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_index = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev_index)
+        # NCCL over NVLink/NVSwitch; UKAN_DIST_BACKEND=gloo lets the multi-rank path be exercised on a
+        # single-GPU box (ranks sharing one device), which NCCL refuses
+        backend = os.environ.get("UKAN_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     try:
         our_arm(args, rank, world, local_rank)
     finally:
