@@ -428,23 +428,35 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   }
 }
 
-__global__ void kan_bwd_tc_reduce_kernel(const double* __restrict__ part, const float* __restrict__ C,
-                                         const float* __restrict__ scale, float* __restrict__ dC,
-                                         float* __restrict__ dscale, int S, int d_in, int d_out, int R) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)d_in * d_out) return;
-  const int i = (int)(t / d_out), o = (int)(t % d_out);
-  const double sc = (double)scale[t];
+// Fixed-order reduction of the split-batch partials + epilogue: CTA = (feature i, 32 outputs);
+// threads sweep the (row, output) pairs (coalesced over o): dC = scale * sum_z part, and the
+// per-row products C * A meet in shared memory for dscale = sum_r C * A (row order).
+__global__ void __launch_bounds__(256) kan_bwd_tc_reduce_kernel(const double* __restrict__ part,
+                                                                const float* __restrict__ C,
+                                                                const float* __restrict__ scale,
+                                                                float* __restrict__ dC, float* __restrict__ dscale,
+                                                                int S, int d_in, int d_out, int R) {
+  extern __shared__ double prod[];  // [R][32]
+  const int i = blockIdx.x, o0 = blockIdx.y * 32;
   const size_t zs = (size_t)d_in * R * d_out;
-  double ds = 0.0;
-  for (int r = 0; r < R; ++r) {
-    const size_t ci = ((size_t)i * R + r) * d_out + o;
-    double a = 0.0;
-    for (int z = 0; z < S; ++z) a += part[z * zs + ci];
-    dC[ci] = (float)(sc * a);
-    ds = fma((double)C[ci], a, ds);
+  for (int p = threadIdx.x; p < R * 32; p += blockDim.x) {
+    const int r = p >> 5, ol = p & 31, o = o0 + ol;
+    double pr = 0.0;
+    if (o < d_out) {
+      const size_t ci = ((size_t)i * R + r) * d_out + o;
+      double a = 0.0;
+      for (int z = 0; z < S; ++z) a += part[z * zs + ci];
+      dC[ci] = (float)((double)scale[(size_t)i * d_out + o] * a);
+      pr = (double)C[ci] * a;
+    }
+    prod[p] = pr;
   }
-  dscale[t] = (float)ds;
+  __syncthreads();
+  if (threadIdx.x < 32 && o0 + threadIdx.x < d_out) {
+    double ds = 0.0;
+    for (int r = 0; r < R; ++r) ds += prod[r * 32 + threadIdx.x];
+    dscale[(size_t)i * d_out + o0 + threadIdx.x] = (float)ds;
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -525,9 +537,8 @@ static int tc2_launch(const float* C, const float* scale, const float* gy, float
                                    p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
-    const int64_t n = (int64_t)d_in * d_out;
-    kan_bwd_tc_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, C, scale, dC, dscale, p.S, d_in,
-                                                                          d_out, G + 3);
+    kan_bwd_tc_reduce_kernel<<<dim3(d_in, (d_out + 31) / 32), 256, sizeof(double) * (G + 3) * 32, st>>>(
+        part, C, scale, dC, dscale, p.S, d_in, d_out, G + 3);
     UKAN_LAUNCH_CHECK();
   }
   return UKAN_OK;
@@ -544,9 +555,8 @@ static int tc_launch(const float* C, const float* scale, const float* gy, float*
                                    p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
-    const int64_t n = (int64_t)d_in * d_out;
-    kan_bwd_tc_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, C, scale, dC, dscale, p.S, d_in,
-                                                                          d_out, G + 3);
+    kan_bwd_tc_reduce_kernel<<<dim3(d_in, (d_out + 31) / 32), 256, sizeof(double) * (G + 3) * 32, st>>>(
+        part, C, scale, dC, dscale, p.S, d_in, d_out, G + 3);
     UKAN_LAUNCH_CHECK();
   }
   return UKAN_OK;
