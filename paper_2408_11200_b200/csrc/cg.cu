@@ -31,7 +31,7 @@ static int dmma_with_ws(const float* A, int64_t sam, int64_t sak, const float* B
                         int64_t N, int64_t K, float* C, cudaStream_t st) {
   const int64_t nb = cg_dmma_workspace(M, N, K);
   void* part = nullptr;  // split-K partials: stream-ordered allocation, no host sync
-  if (nb > 0) UKAN_CUDA_TRY(cudaMallocAsync(&part, (size_t)nb, st));
+  if (nb > 0) UKAN_CUDA_TRY(scratch_alloc(&part, (size_t)nb, st));
   const int rc = cg_dmma_gemm(A, sam, sak, Bm, sbk, sbn, M, N, K, C, static_cast<double*>(part), st);
   if (part) cudaFreeAsync(part, st);
   return rc;

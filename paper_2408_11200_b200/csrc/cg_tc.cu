@@ -355,7 +355,7 @@ int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st)
   const int S = (int)std::max<int64_t>(1, std::min<int64_t>((4 * kan_num_sms() + cblk - 1) / cblk, (K + 255) / 256));
   const int rps = (int)((K + S - 1) / S);
   void* part = nullptr;
-  UKAN_CUDA_TRY(cudaMallocAsync(&part, sizeof(double) * S * N, st));
+  UKAN_CUDA_TRY(scratch_alloc(&part, sizeof(double) * S * N, st));
   cg_colsum_part_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
   UKAN_LAUNCH_CHECK();
   cg_colsum_final_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(static_cast<double*>(part), out, (int)N, S);

@@ -27,6 +27,11 @@ extern "C" void ukan_note_launch(void);
 
 namespace ukan {
 
+// Stream-ordered scratch for the convenience entry points that take no caller workspace.  The
+// device's default pool keeps its memory mapped (release threshold raised once), so repeated
+// calls do not remap pages at every synchronisation.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+
 constexpr int kMaxK = UKAN_MAX_DEGREE + 1;
 
 // Basis matrix passed by value as a kernel parameter (<= 11*11 doubles).

@@ -692,7 +692,7 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
   // Convenience entry without a caller workspace: a stream-ordered allocation (no host sync).
   const int64_t nbytes = base_weight ? 0 : ukan_kan_forward_workspace_size(B, d_in, d_out, G, k);
   void* ws = nullptr;
-  if (nbytes > 0) UKAN_CUDA_TRY(cudaMallocAsync(&ws, (size_t)nbytes, (cudaStream_t)stream));
+  if (nbytes > 0) UKAN_CUDA_TRY(scratch_alloc(&ws, (size_t)nbytes, (cudaStream_t)stream));
   const int rc = ukan_kan_forward_ws(x, coeffs, scale, base_weight, y, B, d_in, d_out, G, k, g_min, g_max,
                                      err_flag, ws, nbytes, stream);
   if (ws) cudaFreeAsync(ws, (cudaStream_t)stream);

@@ -149,6 +149,22 @@ extern "C" int ukan_fill_f32(float* p, int64_t n, float value, void* stream) {
 
 extern "C" int ukan_version(void) { return 100; }
 
+namespace ukan {
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static const bool once = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)once;
+  return cudaMallocAsync(p, bytes, st);
+}
+}  // namespace ukan
+
 static std::atomic<int64_t> g_launches{0};
 extern "C" void ukan_note_launch(void) { g_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" int64_t ukan_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
