@@ -98,6 +98,17 @@ int ukan_kan_locate(const float* x, int32_t* cell, double* u,
                     int64_t B, int64_t d_in, int64_t G, double g_min, double g_max,
                     void* stream);
 
+/* Naive comparison arm (naive_kan_forward, layers.py:321-370): all G+k bases per input by the
+ * Cox-de Boor recursion over the full knot vector, dotted with the whole coefficient table.
+ * tmp [B, d_in, d_out] receives sum_s B_s C[i,s,o] (needed by the backward).  The backward
+ * writes dcoeffs / dscale only (no dx, as the reference arm). */
+int ukan_kan_naive_forward(const float* x, const float* coeffs, const float* scale, float* y,
+                           float* tmp, int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
+                           double g_min, double g_max, void* stream);
+int ukan_kan_naive_backward(const float* x, const float* scale, const float* tmp, const float* gy,
+                            float* dcoeffs, float* dscale, int64_t B, int64_t d_in, int64_t d_out,
+                            int64_t G, int k, double g_min, double g_max, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * UKAN layer (unbounded grid, coefficient generator).  Replaces ukan_forward
  * (layers.py:254-291), _cg_eval (232-243) and positional_encoding (112-123).

@@ -6,7 +6,8 @@ from .bspline import BasisMatrix, basis_matrix
 from .errors import (ConfigError, ContractError, DimensionError, DivergedError, DomainError,
                      FormatError, UkanError)
 from .layers import (KanLayer, LinearLayer, Model, UkanLayer, build_model, cg_coefficients,
-                     init_layer, kan_forward, positional_encoding, select_window, ukan_forward)
+                     init_layer, kan_forward, naive_kan_forward, positional_encoding, select_window,
+                     ukan_forward)
 from .optim import AdamState, LrSchedule, adam_step, lr_at, sgd_step
 from .ops import flush_checks, set_check_mode
 from .train import GradSync, SplineTrainer, shard_bounds

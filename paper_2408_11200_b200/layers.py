@@ -174,6 +174,20 @@ def kan_forward(layer: KanLayer, x) -> torch.Tensor:
                                  float(layer.g_min), float(layer.g_max))
 
 
+def naive_kan_forward(layer: KanLayer, x) -> torch.Tensor:
+    """Same contract as kan_forward computed the slow way (layers.py:337-370): all G+k basis
+    functions per input dotted with the full coefficient table; parameter gradients only.
+    The comparison arm of the grid-size benchmark (``bench_arms.run_bench``)."""
+    x = as_input(x, layer.coeffs.device)
+    if x.ndim != 2 or x.shape[1] != layer.d_in:
+        raise DimensionError(f"expected [batch, {layer.d_in}] input, got {tuple(x.shape)}")
+    y = ops.NaiveKanFn.apply(x.detach(), layer.coeffs, layer.scale, layer.G, layer.k, float(layer.g_min),
+                             float(layer.g_max))
+    if layer.base_weight is not None:
+        y = y + torch.nn.functional.silu(x) @ layer.base_weight
+    return y
+
+
 def _cg_table(layer: UkanLayer, keys: ops.UkanKeys) -> torch.Tensor:
     return ops.CgMlpFn.apply(layer.feature_embedding, layer.cg_w1, layer.cg_b1, layer.cg_w2, layer.cg_b2,
                              keys.key_f, keys.key_g, keys.seg_start, layer.d_pe)

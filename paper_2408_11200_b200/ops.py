@@ -102,6 +102,41 @@ class KanSplineFn(torch.autograd.Function):
         return dx, dC, ds, dbw, None, None, None, None
 
 
+class NaiveKanFn(torch.autograd.Function):
+    """naive_kan_forward (layers.py:337-370): all G+k bases by Cox-de Boor, dotted with the whole
+    coefficient table (the grid-size benchmark's comparison arm).  Backward covers the parameters
+    only, as the reference."""
+
+    @staticmethod
+    def forward(ctx, x, coeffs, scale, G: int, k: int, g_min: float, g_max: float):
+        lib = _lib.load()
+        _lib.require_cuda(x, coeffs, scale)
+        x = _f32(x)
+        B, d_in = x.shape
+        d_out = coeffs.shape[2]
+        y = torch.empty((B, d_out), device=x.device, dtype=torch.float32)
+        tmp = torch.empty((B, d_in, d_out), device=x.device, dtype=torch.float32)
+        check(lib.ukan_kan_naive_forward(ptr(x), ptr(coeffs), ptr(scale), ptr(y), ptr(tmp), B, d_in, d_out, G, k,
+                                         g_min, g_max, stream_ptr()), "naive_kan_forward")
+        ctx.save_for_backward(x, scale, tmp)
+        ctx.meta = (G, k, float(g_min), float(g_max), tuple(coeffs.shape))
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        lib = _lib.load()
+        x, scale, tmp = ctx.saved_tensors
+        G, k, g_min, g_max, cshape = ctx.meta
+        gy = _f32(gy)
+        B, d_in = x.shape
+        d_out = cshape[2]
+        dC = torch.empty(cshape, device=x.device, dtype=torch.float32)
+        ds = torch.empty_like(scale)
+        check(lib.ukan_kan_naive_backward(ptr(x), ptr(scale), ptr(tmp), ptr(gy), ptr(dC), ptr(ds), B, d_in, d_out, G,
+                                          k, g_min, g_max, stream_ptr()), "naive_kan_backward")
+        return None, dC, ds, None, None, None, None
+
+
 def kan_locate(x: torch.Tensor, G: int, g_min: float, g_max: float):
     """(cell int32, u float64) exactly as layers.py:296-300 — for parity tooling."""
     lib = _lib.load()
