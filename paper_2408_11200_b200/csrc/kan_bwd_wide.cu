@@ -1,0 +1,302 @@
+// kan_bwd_wide.cu — KAN backward (table side) for fine grids: cost independent of G.
+//
+// Replaces the bwd closures of span_gather (layers.py:67-70, the np.add.at scatter of the window
+// gradient), edge_combine (84-88) and the base branch (layers.py:310-316) when the grid is too
+// fine for the register / tensor-core sweeps (kan_bwd.cu, kan_bwd_tc.cu: G <= ~64), which is the
+// regime of the paper's grid-size benchmark (bench.py:76-96, G up to thousands):
+//   A[i,r,o] = sum_{(b,j): cell_bi + j = r} w_j(u_bi) * g[b,o]     (fp64)
+//   dC = scale * A,   dscale = sum_r C * A,   dbw = sum_b silu(x) * g.
+// Every sample touches K of the R = G + k rows, so the work is O(B * d_in * K * d_out) plus the
+// unavoidable R * d_in * d_out writes of dC — flat in G, like the matrix-form forward.
+//
+//  * prep: one warp per (feature, 256-sample chunk): fp64 locate (layers.py:299-300), a rank sort
+//    of the chunk by key (cell << 8 | sample) (keys are unique -> stable, deterministic), and the
+//    start of every 32-row tile in the sorted chunk.  Records stay L2-resident.
+//  * sweep: one warp per (feature, 32-row tile, 32-output slice), lane = output.  For each chunk
+//    it walks only the samples whose window meets its tile (cells [r0-k, r0+31]), evaluates the
+//    basis weights lane-parallel (one sample per lane), then runs the samples in sorted order,
+//    keeping the window of the current cell in K registers and flushing it into a 32x32 fp64
+//    shared-memory tile when the cell changes.  dC and the tile's dscale partial are written
+//    once at the end; a second kernel sums the dscale partials over tiles in fixed order.
+// Deterministic: fixed chunk order, cell-then-sample order inside a chunk, fixed reductions.
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+
+namespace ukan {
+
+constexpr int kWdBC = 256;       // samples per chunk (sample index packed in 8 bits)
+constexpr int kWdRT = 32;        // rows per tile
+constexpr int kWdMaxTiles = 1024;
+constexpr int kWdBadCell = (1 << 23) - 1;  // > any valid cell (check_kan_args: G + k < 2^23)
+
+struct WidePlan {
+  bool ok = false;
+  int n_rt = 0, n_os = 0, nch = 0, st_n = 0;
+  size_t recb = 0;
+  int64_t rec_bytes = 0, part_bytes = 0;
+};
+
+// record layout per (feature, chunk), 16-B aligned: key[256] int | u[256] double | st[st_n] int
+__host__ __device__ constexpr int wide_warp_doubles(int K) { return kWdRT * 32 + 32 * K + 32; }
+
+static size_t wide_rec_bytes(int st_n) { return (size_t)kWdBC * 12 + (size_t)st_n * 4; }
+
+__global__ void __launch_bounds__(256)
+kan_bwd_wide_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ recs, int B, int d_in, int nch,
+                         int n_rt, int st_n, size_t recb, KanGrid grid) {
+  __shared__ float xs[kWdBC][9];
+  __shared__ __align__(16) int keys[8][kWdBC];
+  __shared__ int sorted[8][kWdBC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * 8, n = blockIdx.y;
+  const int b0 = n * kWdBC;
+  const int nb = min(kWdBC, B - b0);
+  for (int t = threadIdx.x; t < kWdBC * 8; t += blockDim.x) {
+    const int s = t / 8, f = t % 8;
+    xs[s][f] = (s < nb && i0 + f < d_in) ? x[(size_t)(b0 + s) * d_in + i0 + f] : 0.f;
+  }
+  __syncthreads();
+  const int i = i0 + warp;
+  if (i >= d_in) return;
+  unsigned char* rec = recs + ((size_t)i * nch + n) * recb;
+  int* ent = reinterpret_cast<int*>(rec);
+  double* uu = reinterpret_cast<double*>(rec + kWdBC * 4);
+  int* st = reinterpret_cast<int*>(rec + kWdBC * 12);
+  constexpr int PER = kWdBC / 32;
+  int key[PER];
+  double us[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int s = q * 32 + lane;
+    int cell = kWdBadCell;
+    double u = 0.0;
+    bool mask;
+    if (s < nb && !kan_locate(xs[s][warp], grid, cell, u, mask)) cell = kWdBadCell;  // NaN: no contribution
+    key[q] = (cell << 8) | s;
+    us[q] = u;
+    keys[warp][s] = key[q];
+  }
+  __syncwarp();
+  int rank[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) rank[q] = 0;
+  const int4* k4 = reinterpret_cast<const int4*>(keys[warp]);
+  for (int m = 0; m < kWdBC / 4; ++m) {
+    const int4 v = k4[m];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      rank[q] += (v.x < key[q]) + (v.y < key[q]) + (v.z < key[q]) + (v.w < key[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    sorted[warp][rank[q]] = key[q];
+    ent[rank[q]] = key[q];
+    uu[rank[q]] = us[q];
+  }
+  __syncwarp();
+  // st[t] = number of keys with cell < 32 t  (t = 0 .. n_rt), lower bound by binary search
+  for (int t = lane; t < st_n; t += 32) {
+    const int tt = min(t, n_rt);
+    const int kk = (tt * kWdRT) << 8;
+    int lo = 0, hi = kWdBC;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sorted[warp][mid] < kk) lo = mid + 1;
+      else hi = mid;
+    }
+    st[t] = lo;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+kan_bwd_wide_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
+                          const float* __restrict__ scale, const float* __restrict__ gy, float* __restrict__ dC,
+                          double* __restrict__ part, int d_in, int d_out, int R, int n_rt, int n_os, int nch,
+                          size_t recb, Basis<K> bas) {
+  extern __shared__ __align__(16) double wsm[];  // per warp: A[32][32] | wb[32][K] | cb[32] bb[32] (int)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double (*A)[32] = reinterpret_cast<double (*)[32]>(wsm + (size_t)warp * wide_warp_doubles(K));
+  double (*wb)[K] = reinterpret_cast<double (*)[K]>(&A[kWdRT][0]);
+  int* cb = reinterpret_cast<int*>(&wb[32][0]);
+  int* bb = cb + 32;
+  const int64_t unit = (int64_t)blockIdx.x * 8 + warp;
+  if (unit >= (int64_t)d_in * n_rt * n_os) return;
+  const int t = (int)(unit % n_rt);
+  const int64_t rest = unit / n_rt;
+  const int os = (int)(rest % n_os);
+  const int i = (int)(rest / n_os);
+  const int o = os * 32 + lane;
+  const bool live = o < d_out;
+  const int r0 = t * kWdRT;
+  const int lo_cell = r0 - (K - 1);
+#pragma unroll 4
+  for (int r = 0; r < kWdRT; ++r) A[r][lane] = 0.0;
+
+  double acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = 0.0;
+  int cur = INT_MIN;
+  auto flush = [&]() {
+    if (cur != INT_MIN) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int r = cur + j - r0;
+        if (r >= 0 && r < kWdRT) A[r][lane] += acc[j];
+        acc[j] = 0.0;
+      }
+    }
+  };
+
+  for (int c = 0; c < nch; ++c) {
+    const unsigned char* rec = recs + ((size_t)i * nch + c) * recb;
+    const int* ent = reinterpret_cast<const int*>(rec);
+    const double* uu = reinterpret_cast<const double*>(rec + kWdBC * 4);
+    const int* st = reinterpret_cast<const int*>(rec + kWdBC * 12);
+    int lo = __ldg(st + t);
+    const int hi = __ldg(st + t + 1);
+    // extend backwards over the cells r0-k .. r0-1 whose windows reach into this tile
+    while (lo > 0) {
+      const int idx = lo - 32 + lane;
+      const bool ok = idx >= 0 && (__ldg(ent + idx) >> 8) >= lo_cell;
+      const int nk = __popc(__ballot_sync(0xffffffffu, ok));
+      lo -= nk;
+      if (nk < 32) break;
+    }
+    for (int p0 = lo; p0 < hi; p0 += 32) {
+      const int p = p0 + lane;
+      if (p < hi) {
+        const int key = __ldg(ent + p);
+        double w[K];
+        basis_weights<K>(bas, __ldg(uu + p), w);
+#pragma unroll
+        for (int j = 0; j < K; ++j) wb[lane][j] = w[j];
+        cb[lane] = key >> 8;
+        bb[lane] = c * kWdBC + (key & 255);
+      }
+      __syncwarp();
+      const int ns = min(32, hi - p0);
+      float gv[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        gv[q] = (q < ns && live) ? __ldg(gy + (size_t)bb[q] * d_out + o) : 0.f;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        if (q < ns) {
+          const int cell = cb[q];
+          if (cell != cur) {
+            flush();
+            cur = cell;
+          }
+          const double g = (double)gv[q];
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[j] = fma(wb[q][j], g, acc[j]);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  flush();
+  __syncwarp();
+  double prod = 0.0;
+  if (live) {
+    const double sc = (double)__ldg(scale + (size_t)i * d_out + o);
+    for (int r = 0; r < kWdRT; ++r) {
+      const int row = r0 + r;
+      if (row >= R) break;
+      const double a = A[r][lane];
+      const size_t ci = ((size_t)i * R + row) * d_out + o;
+      dC[ci] = (float)(sc * a);
+      prod = fma((double)__ldg(C + ci), a, prod);
+    }
+    part[((size_t)i * n_rt + t) * d_out + o] = prod;
+  }
+}
+
+// dscale[i,o] = sum_t part[i][t][o]  (fixed tile order)
+__global__ void kan_bwd_wide_reduce_kernel(const double* __restrict__ part, float* __restrict__ dscale, int d_in,
+                                           int d_out, int n_rt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)d_in * d_out) return;
+  const int i = (int)(e / d_out), o = (int)(e % d_out);
+  double a = 0.0;
+  for (int t = 0; t < n_rt; ++t) a += part[((size_t)i * n_rt + t) * d_out + o];
+  dscale[e] = (float)a;
+}
+
+// dbw[i,o] = sum_b silu(x[b,i]) g[b,o]  (fp64, sample order).  Warp = feature, lane = output;
+// the 8 warps of a CTA share g rows through L1.
+__global__ void __launch_bounds__(256)
+kan_dbase_kernel(const float* __restrict__ x, const float* __restrict__ gy, float* __restrict__ dbw, int B,
+                 int d_in, int d_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp, o = blockIdx.y * 32 + lane;
+  if (i >= d_in) return;
+  double a = 0.0;
+  for (int b0 = 0; b0 < B; b0 += 32) {
+    const int b = b0 + lane;
+    const double s = b < B ? silu_d((double)__ldg(x + (size_t)b * d_in + i)) : 0.0;
+    const int nb = min(32, B - b0);
+    for (int q = 0; q < nb; ++q) {
+      const double sq = __shfl_sync(0xffffffffu, s, q);
+      if (o < d_out) a = fma(sq, (double)__ldg(gy + (size_t)(b0 + q) * d_out + o), a);
+    }
+  }
+  if (o < d_out) dbw[(size_t)i * d_out + o] = (float)a;
+}
+
+WidePlan kan_bwd_wide_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K) {
+  WidePlan p;
+  if (B < 1 || K < 1 || K > kMaxK) return p;
+  p.n_rt = (R + kWdRT - 1) / kWdRT;
+  if (p.n_rt > kWdMaxTiles) return p;
+  p.n_os = (int)((d_out + 31) / 32);
+  p.nch = (int)((B + kWdBC - 1) / kWdBC);
+  p.st_n = ((p.n_rt + 1 + 3) / 4) * 4;
+  p.recb = wide_rec_bytes(p.st_n);
+  p.rec_bytes = (int64_t)d_in * p.nch * (int64_t)p.recb;
+  p.part_bytes = (int64_t)sizeof(double) * d_in * p.n_rt * d_out;
+  p.ok = true;
+  return p;
+}
+
+int64_t kan_bwd_wide_workspace(const WidePlan& p) {
+  return p.ok ? ((p.rec_bytes + 255) / 256) * 256 + p.part_bytes : 0;
+}
+
+template <int K>
+int kan_bwd_wide_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                     float* dbw, void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int R,
+                     const KanGrid& grid, const WidePlan& p, cudaStream_t st) {
+  if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_wide_workspace(p)) return UKAN_E_WORKSPACE;
+  unsigned char* recs = reinterpret_cast<unsigned char*>(workspace);
+  double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
+  kan_bwd_wide_prep_kernel<<<dim3((d_in + 7) / 8, p.nch), 256, 0, st>>>(x, recs, B, d_in, p.nch, p.n_rt, p.st_n,
+                                                                         p.recb, grid);
+  UKAN_LAUNCH_CHECK();
+  const int64_t units = (int64_t)d_in * p.n_rt * p.n_os;
+  const size_t smem = sizeof(double) * 8 * (size_t)wide_warp_doubles(K);
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kan_bwd_wide_sweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kan_bwd_wide_sweep_kernel<K><<<(unsigned)((units + 7) / 8), 256, smem, st>>>(
+      recs, C, scale, gy, dC, part, d_in, d_out, R, p.n_rt, p.n_os, p.nch, p.recb, make_basis<K>(K - 1));
+  UKAN_LAUNCH_CHECK();
+  const int64_t n = (int64_t)d_in * d_out;
+  kan_bwd_wide_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, dscale, d_in, d_out, p.n_rt);
+  UKAN_LAUNCH_CHECK();
+  if (dbw) {
+    kan_dbase_kernel<<<dim3((d_in + 7) / 8, (d_out + 31) / 32), 256, 0, st>>>(x, gy, dbw, B, d_in, d_out);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
+
+#define UKAN_WIDE_INST(K)                                                                                     \
+  template int kan_bwd_wide_run<K>(const float*, const float*, const float*, const float*, float*, float*,   \
+                                   float*, void*, int64_t, int, int, int, int, const KanGrid&, const WidePlan&, \
+                                   cudaStream_t);
+UKAN_WIDE_INST(1) UKAN_WIDE_INST(2) UKAN_WIDE_INST(3) UKAN_WIDE_INST(4) UKAN_WIDE_INST(5) UKAN_WIDE_INST(6)
+UKAN_WIDE_INST(7) UKAN_WIDE_INST(8) UKAN_WIDE_INST(9) UKAN_WIDE_INST(10) UKAN_WIDE_INST(11)
+
+}  // namespace ukan

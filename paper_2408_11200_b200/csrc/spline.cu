@@ -534,6 +534,18 @@ int kan_fwd_narrow(const float* x, const float* C, const float* scale, const flo
 template <int K>
 int kan_dx_narrow2(const float* x, const float* C, const float* scale, const float* bw, const float* gy, float* dx,
                    int B, int d_in, int d_out, int R, const KanGrid& grid, cudaStream_t st);
+struct WidePlan {
+  bool ok = false;
+  int n_rt = 0, n_os = 0, nch = 0, st_n = 0;
+  size_t recb = 0;
+  int64_t rec_bytes = 0, part_bytes = 0;
+};
+WidePlan kan_bwd_wide_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K);
+int64_t kan_bwd_wide_workspace(const WidePlan& p);
+template <int K>
+int kan_bwd_wide_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                     float* dbw, void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int R,
+                     const KanGrid& grid, const WidePlan& p, cudaStream_t st);
 template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
@@ -707,6 +719,9 @@ extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int
   const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, (int)(G + k), k + 1, true, kan_num_sms());
   const int64_t tc = kan_bwd_tc_workspace(kan_bwd_tc_plan(B, d_in, d_out, G, k, false));
   const int64_t sw = kan_bwd_sw_workspace(kan_bwd_sw_plan(B, d_in, d_out, (int)(G + k), k + 1, true));
+  const int64_t wd = kan_bwd_wide_workspace(kan_bwd_wide_plan(B, d_in, d_out, (int)(G + k), k + 1));
+  static const bool force_wide = getenv("UKAN_BWD") && getenv("UKAN_BWD")[0] == 'w';
+  if ((!p.ok || force_wide) && wd > 0) return std::max<int64_t>(wd, p.ok ? p.ws_bytes : 0);
   if (p.ok) return std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc), sw);
   if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
@@ -747,6 +762,25 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
     if (tp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_tc_workspace(tp)) {
       int rc = kan_bwd_tc_run(x, coeffs, scale, gy, dC, dscale, workspace, workspace_bytes, B, d_in, d_out,
                               rm.R - K + 1, rm.grid, tp, st);
+      if (rc) return rc;
+      if (dx) {
+        if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+        const Basis<K> bas = make_basis<K>(K - 1);
+        const int64_t pairs = (int64_t)B * d_in;
+        spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
+                                                                               d_out, rm, bas);
+        UKAN_LAUNCH_CHECK();
+      }
+      return UKAN_OK;
+    }
+  }
+  // Fine grids (R > 72 or K > 6, outside the register sweep) or UKAN_BWD=wide: sorted-chunk
+  // sweep whose cost does not grow with G (kan_bwd_wide.cu).
+  if (B > 0 && (sel[0] == 'w' || !kan_bwd_reg_plan(B, d_in, d_out, rm.R, K, bw != nullptr, kan_num_sms()).ok)) {
+    const WidePlan wp = kan_bwd_wide_plan(B, d_in, d_out, rm.R, K);
+    if (wp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_wide_workspace(wp)) {
+      int rc = kan_bwd_wide_run<K>(x, coeffs, scale, gy, dC, dscale, dbw, workspace, workspace_bytes, B, d_in, d_out,
+                                   rm.R, rm.grid, wp, st);
       if (rc) return rc;
       if (dx) {
         if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
@@ -800,7 +834,10 @@ extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const f
   rm.grid = make_kan_grid(g_min, g_max, G);
   rm.R = (int)(G + k);
   const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, rm.R, k + 1, base_weight != nullptr, kan_num_sms());
-  if (!p.ok && !bwd_fits_smem(k + 1, rm.R) &&
+  const WidePlan wp = kan_bwd_wide_plan(B, d_in, d_out, rm.R, k + 1);
+  if (!p.ok && wp.ok && B > 0 && (workspace == nullptr || workspace_bytes < kan_bwd_wide_workspace(wp)))
+    return UKAN_E_WORKSPACE;
+  if (!p.ok && !wp.ok && !bwd_fits_smem(k + 1, rm.R) &&
       (workspace == nullptr || workspace_bytes < (int64_t)sizeof(double) * d_in * rm.R * d_out))
     return UKAN_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
@@ -813,9 +850,14 @@ extern "C" int ukan_kan_backward(const float* x, const float* coeffs, const floa
                                  float* dcoeffs, float* dscale, float* dbase_weight, int64_t B,
                                  int64_t d_in, int64_t d_out, int64_t G, int k, double g_min,
                                  double g_max, void* stream) {
-  return ukan_kan_backward_ws(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale,
-                              dbase_weight, B, d_in, d_out, G, k, g_min, g_max, nullptr, 0,
-                              stream);
+  // Convenience entry without a caller workspace: a stream-ordered allocation (no host sync).
+  const int64_t nbytes = ukan_kan_backward_workspace_size(B, d_in, d_out, G, k);
+  void* ws = nullptr;
+  if (nbytes > 0 && B > 0) UKAN_CUDA_TRY(scratch_alloc(&ws, (size_t)nbytes, (cudaStream_t)stream));
+  const int rc = ukan_kan_backward_ws(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, B, d_in,
+                                      d_out, G, k, g_min, g_max, ws, ws ? nbytes : 0, stream);
+  if (ws) cudaFreeAsync(ws, (cudaStream_t)stream);
+  return rc;
 }
 
 extern "C" int ukan_kan_locate(const float* x, int32_t* cell, double* u, int64_t B,

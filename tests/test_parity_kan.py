@@ -167,3 +167,30 @@ def test_full_size_checksums(B, d_in, d_out, G):
     lhs2 = (sc * layer.scale.grad.double()).sum(dim=0)
     rhs2 = (g64 * y.detach().double()).sum(dim=0)
     assert_close(lhs2.cpu().numpy(), rhs2.cpu().numpy(), rtol=1e-4, atol=1e-3, what="scale.dscale")
+
+
+@pytest.mark.parametrize("B,d_in,d_out,k,G,base", [(1000, 6, 40, 3, 200, True), (513, 5, 70, 7, 150, False),
+                                                   (300, 3, 10, 10, 90, True), (257, 2, 33, 0, 3000, False)])
+def test_fine_grid_sorted_sweep(B, d_in, d_out, k, G, base):
+    """Fine grids (R > 72 or K > 6) run the sorted-chunk sweep (kan_bwd_wide.cu)."""
+    check_against_oracle(*random_case(B, d_in, d_out, k, G, seed=20 + k, outliers=0.05, base=base))
+
+
+def test_fine_grid_clustered_cells():
+    """Hundreds of samples per cell just below a 32-row tile boundary: the backward extension
+    over cells r0-k..r0-1 must walk more than one 32-entry step, and chunk-crossing runs of one
+    cell must accumulate in order."""
+    layer, x, gup = random_case(1500, 3, 36, 3, 1000, seed=31)
+    dg = 2.0 / 1000
+    rng = np.random.default_rng(32)
+    cells = rng.choice([30, 31, 62, 63, 64, 999], size=x.shape)
+    x[:] = (-1.0 + (cells + rng.uniform(0.1, 0.9, x.shape)) * dg).astype(np.float32)
+    check_against_oracle(layer, x, gup)
+    layer.coeffs.grad = None
+    layer.scale.grad = None
+    a = run_layer(layer, x, gup)
+    layer.coeffs.grad = None
+    layer.scale.grad = None
+    b = run_layer(layer, x, gup)
+    for key in a:
+        np.testing.assert_array_equal(a[key], b[key])
