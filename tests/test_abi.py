@@ -58,7 +58,10 @@ def test_basis_matrix_rejects_bad_degree():
 def test_workspace_queries():
     lib = _lib.load()
     assert lib.ukan_kan_backward_workspace_size(1024, 64, 64, 10, 3) >= 0
-    assert lib.ukan_kan_backward_workspace_size(4096, 32, 32, 4096, 3) == 8 * 32 * 4099 * 32  # G beyond the register path
+    # G beyond the register path: chunk records (256 samples: keys, u, 32-row tile starts) + dscale partials
+    n_rt = (4099 + 31) // 32
+    recb = 256 * 12 + (n_rt + 1 + 3) // 4 * 4 * 4
+    assert lib.ukan_kan_backward_workspace_size(4096, 32, 32, 4096, 3) == 32 * 16 * recb + 8 * 32 * n_rt * 32
     assert lib.ukan_ukan_keys_workspace_size(100, 10, 1000) > 2 * 1000 * 8
     assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == 8 * 10 * 4 * 3
 
