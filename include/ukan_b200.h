@@ -109,6 +109,19 @@ int ukan_kan_naive_backward(const float* x, const float* scale, const float* tmp
                             float* dcoeffs, float* dscale, int64_t B, int64_t d_in, int64_t d_out,
                             int64_t G, int k, double g_min, double g_max, void* stream);
 
+/* Forward tangent (JVP) of the KAN layer and its backward (the tangent channel of
+ * basis_features / edge_combine / clamp / silu, layers.py:49-53, 91-104, tensor.py:236-241,
+ * 336-337, used by pinn_loss, tasks.py:153-166).  ty = (dy/dx) . tx per sample.  The backward
+ * WRITES the gradients of sum(ty * gt): dx (tangent path only, nullable), dtx (nullable),
+ * dcoeffs, dscale, dbase_weight (iff base_weight).  fp64 evaluation and sums, deterministic. */
+int ukan_kan_jvp_forward(const float* x, const float* tx, const float* coeffs, const float* scale,
+                         const float* base_weight, float* ty, int64_t B, int64_t d_in, int64_t d_out,
+                         int64_t G, int k, double g_min, double g_max, void* stream);
+int ukan_kan_jvp_backward(const float* x, const float* tx, const float* coeffs, const float* scale,
+                          const float* base_weight, const float* gt, float* dx, float* dtx,
+                          float* dcoeffs, float* dscale, float* dbase_weight, int64_t B, int64_t d_in,
+                          int64_t d_out, int64_t G, int k, double g_min, double g_max, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * UKAN layer (unbounded grid, coefficient generator).  Replaces ukan_forward
  * (layers.py:254-291), _cg_eval (232-243) and positional_encoding (112-123).
@@ -185,6 +198,18 @@ int ukan_ukan_backward(const float* x, const int32_t* base_row, const int32_t* s
                        int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int k,
                        double delta_g, void* workspace, int64_t workspace_bytes,
                        void* stream);
+
+/* Forward tangent of the UKAN spline over the generated table (u = x/dg - g_id carries tx/dg,
+ * layers.py:264; the table has no tangent) and its backward: dx (tangent share, nullable), dtx
+ * (nullable), dtable [n_u*K, d_out] (written), dscale (written).  Same key layout as above. */
+int ukan_ukan_jvp_forward(const float* x, const float* tx, const int32_t* base_row, const float* table,
+                          const float* scale, float* ty, int64_t B, int64_t d_in, int64_t d_out, int k,
+                          double delta_g, void* stream);
+int ukan_ukan_jvp_backward(const float* x, const float* tx, const int32_t* base_row,
+                           const int32_t* seg_start, const float* table, const float* scale,
+                           const float* gt, float* dx, float* dtx, float* dtable, float* dscale,
+                           int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int k, double delta_g,
+                           void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Training-step kernels (train.py:142-150, optim.py:31-54, tensor.py:368-400).

@@ -159,6 +159,22 @@ def cg_forward(keys, d_in, emb, w1, b1, w2, b2, d_pe, K, d_out):
     return out.reshape(keys.shape[0], K, d_out), dict(f_idx=f_idx, inp=inp, pre=pre, s=s, H=H)
 
 
+def _cg_backward(c, p, dtable):
+    """Tape backward of _cg_eval (layers.py:232-243) through matmul/silu/gather_rows/concat_last
+    (tensor.py:189-197, 228-233, 257-268, 276-285), given dL/dtable [n, K, d_out]."""
+    dout = dtable.reshape(dtable.shape[0], -1)                            # reshape bwd
+    dw2 = c["H"].T @ dout
+    db2 = dout.sum(axis=0)
+    dH = dout @ p["cg_w2"].T
+    dpre = dH * (c["s"] + c["pre"] * c["s"] * (1.0 - c["s"]))            # tensor.py:233
+    dw1 = c["inp"].T @ dpre
+    db1 = dpre.sum(axis=0)
+    dinp = dpre @ p["cg_w1"].T
+    demb = np.zeros_like(p["feature_embedding"])
+    np.add.at(demb, c["f_idx"], dinp[:, :p["feature_embedding"].shape[1]])  # tensor.py:265-268
+    return dict(dcg_w1=dw1, dcg_b1=db1, dcg_w2=dw2, dcg_b2=db2, dfeature_embedding=demb)
+
+
 def ukan_forward_backward(x, p, gy=None, *, k, delta_g, d_pe, need_dx=True):
     """ukan_forward (layers.py:254-291) + the tape backward through span_gather, the CG MLP
     (matmul/silu/gather_rows/concat_last, tensor.py:189-197, 228-233, 257-268, 276-285).
@@ -180,20 +196,98 @@ def ukan_forward_backward(x, p, gy=None, *, k, delta_g, d_pe, need_dx=True):
     out = dict(y=y, g_id=g_id, uniq=uniq)
     if gy is None:
         return out
-    dout = g["dtable"].reshape(table.shape[0], K * d_out)                 # reshape bwd
-    dw2 = c["H"].T @ dout
-    db2 = dout.sum(axis=0)
-    dH = dout @ p["cg_w2"].T
-    dpre = dH * (c["s"] + c["pre"] * c["s"] * (1.0 - c["s"]))            # tensor.py:233
-    dw1 = c["inp"].T @ dpre
-    db1 = dpre.sum(axis=0)
-    dinp = dpre @ p["cg_w1"].T
-    demb = np.zeros_like(p["feature_embedding"])
-    np.add.at(demb, c["f_idx"], dinp[:, :p["feature_embedding"].shape[1]])  # tensor.py:265-268
-    out.update(dscale=g["dscale"], dcg_w1=dw1, dcg_b1=db1, dcg_w2=dw2, dcg_b2=db2,
-               dfeature_embedding=demb, table=table)
+    out.update(dscale=g["dscale"], table=table, **_cg_backward(c, p, g["dtable"]))
     if need_dx:
         out["dx"] = g["du"] * (1.0 / delta_g)                            # T.mul(x, inv_dg) bwd
+    return out
+
+
+def _silu2(x):
+    """Second derivative of silu, d/dx [s + x s (1 - s)] (the tape derivative of the silu
+    tangent, tensor.py:236-241)."""
+    s = 1.0 / (1.0 + np.exp(-x))
+    return s * (1.0 - s) * (2.0 + x * (1.0 - 2.0 * s))
+
+
+def _spline_tangent(table, rows, cols, u, tu, scale, gt, k):
+    """Forward tangent of span_gather + basis_features + edge_combine when only u carries a
+    tangent tu (basis.tangent = w'(u) * u.tangent, layers.py:49-53; edge_combine of the tangent
+    basis, layers.py:91-104), and the tape backward of sum(ty * gt) through that tangent graph."""
+    windows = table[rows, cols]
+    d1 = basis_values(u, k, 1)
+    bt = d1 * tu[..., None]                                   # layers.py:51-52
+    tmp = np.einsum("bfj,bfjo->bfo", bt, windows)             # layers.py:81 on the tangent basis
+    ty = np.einsum("bfo,fo->bo", tmp, scale)
+    if gt is None:
+        return ty, None
+    dtmp = gt[:, None, :] * scale[None, :, :]
+    dscale = np.einsum("bo,bfo->fo", gt, tmp)
+    dbt = np.einsum("bfo,bfjo->bfj", dtmp, windows)
+    dwin = bt[..., None] * dtmp[:, :, None, :]
+    dtable = np.zeros_like(table)
+    np.add.at(dtable, (rows, cols), dwin)
+    dtu = (dbt * d1).sum(axis=-1)                             # mul bwd into u.tangent
+    du = (dbt * tu[..., None] * basis_values(u, k, 2)).sum(axis=-1)  # basis_features(d=1) bwd
+    return ty, dict(dtable=dtable, dscale=dscale, dtu=dtu, du=du)
+
+
+def kan_tangent_forward_backward(x, tx, coeffs, scale, gy, gt, *, k, g_min, g_max, G, base_weight=None):
+    """kan_forward (layers.py:304-318) on x seeded with the tangent tx (tensor.py:411-424):
+    returns y, ty = dy/dx . tx and the gradients of L = sum(y * gy) + sum(ty * gt) with respect
+    to x, tx, coeffs, scale (and base_weight), as the reference's tape produces them through the
+    tangent graph (clamp tangent tensor.py:336-337, mul(xc, 1/dg) layers.py:300, silu tangent
+    tensor.py:236-241)."""
+    x = np.asarray(x, dtype=np.float64)
+    tx = np.asarray(tx, dtype=np.float64)
+    B, f = x.shape
+    K = k + 1
+    prim = kan_forward_backward(x, coeffs, scale, gy, k=k, g_min=g_min, g_max=g_max, G=G,
+                                base_weight=base_weight, need_dx=True)
+    cell, u, mask = kan_locate(x, g_min, g_max, G)
+    inv = 1.0 / ((g_max - g_min) / G)
+    tu = tx * mask * inv
+    rows = np.broadcast_to(np.arange(f)[None, :, None], (B, f, K))
+    cols = cell[..., None] + np.arange(K)
+    ty, t = _spline_tangent(coeffs, rows, cols, u, tu, scale, gt, k)
+    dx = prim["dx"] + t["du"] * mask * inv
+    dtx = t["dtu"] * mask * inv
+    out = dict(y=prim["y"], cell=cell, dcoeffs=prim["dcoeffs"] + t["dtable"], dscale=prim["dscale"] + t["dscale"])
+    if base_weight is not None:
+        _, dsx = _silu(x)
+        ty = ty + (dsx * tx) @ base_weight
+        gb = gt @ base_weight.T
+        dx = dx + gb * tx * _silu2(x)
+        dtx = dtx + gb * dsx
+        out["dbase_weight"] = prim["dbase_weight"] + (dsx * tx).T @ gt
+    out.update(ty=ty, dx=dx, dtx=dtx)
+    return out
+
+
+def ukan_tangent_forward_backward(x, tx, p, gy, gt, *, k, delta_g, d_pe):
+    """ukan_forward (layers.py:254-291) on x seeded with the tangent tx: u = x*(1/dg) - g_id
+    carries tu = tx/dg (mul tangent, tensor.py:166-177); the generated table has no tangent.
+    Returns y, ty and the gradients of L = sum(y * gy) + sum(ty * gt) for x, tx, scale and the
+    CG parameters (the table gradient of both paths flows through one CG backward)."""
+    x = np.asarray(x, dtype=np.float64)
+    tx = np.asarray(tx, dtype=np.float64)
+    B, f = x.shape
+    K = k + 1
+    d_out = p["scale"].shape[1]
+    uniq, inverse, g_id, u, offset = ukan_keys(x, delta_g, k)
+    n = B * f
+    table, c = cg_forward(uniq, f, p["feature_embedding"], p["cg_w1"], p["cg_b1"], p["cg_w2"],
+                          p["cg_b2"], d_pe, K, d_out)
+    idx_prev = inverse[:n].reshape(B, f)
+    idx_next = inverse[n:].reshape(B, f)
+    col = offset[..., None] + np.arange(K)
+    rows = np.where(col < K, idx_prev[..., None], idx_next[..., None])
+    cols = col % K
+    inv = 1.0 / delta_g
+    y, g = _spline_fwd_bwd(table, rows, cols, u, p["scale"], gy, k, True)
+    ty, t = _spline_tangent(table, rows, cols, u, tx * inv, p["scale"], gt, k)
+    out = dict(y=y, ty=ty, g_id=g_id, dscale=g["dscale"] + t["dscale"], dx=(g["du"] + t["du"]) * inv,
+               dtx=t["dtu"] * inv)
+    out.update(_cg_backward(c, p, g["dtable"] + t["dtable"]))
     return out
 
 

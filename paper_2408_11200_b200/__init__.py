@@ -6,10 +6,11 @@ from .bspline import BasisMatrix, basis_matrix
 from .errors import (ConfigError, ContractError, DimensionError, DivergedError, DomainError,
                      FormatError, UkanError)
 from .layers import (KanLayer, LinearLayer, Model, UkanLayer, build_model, cg_coefficients,
-                     init_layer, kan_forward, naive_kan_forward, positional_encoding, select_window,
-                     ukan_forward)
+                     init_layer, kan_forward, kan_forward_tangent, naive_kan_forward, positional_encoding, select_window,
+                     ukan_forward, ukan_forward_tangent)
 from .optim import AdamState, LrSchedule, adam_step, lr_at, sgd_step
 from .ops import flush_checks, set_check_mode
+from .pinn import PinnProblem, pinn_loss
 from .train import GradSync, SplineTrainer, shard_bounds
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -98,6 +98,9 @@ class KanLayer:
     def forward(self, x):
         return kan_forward(self, x)
 
+    def forward_tangent(self, x, tx):
+        return kan_forward_tangent(self, x, tx)
+
     __call__ = forward
 
 
@@ -140,6 +143,9 @@ class UkanLayer:
 
     def forward(self, x):
         return ukan_forward(self, x)
+
+    def forward_tangent(self, x, tx):
+        return ukan_forward_tangent(self, x, tx)
 
     __call__ = forward
 
@@ -206,6 +212,36 @@ def ukan_forward(layer: UkanLayer, x, dedup: bool = True) -> torch.Tensor:
                                   float(layer.delta_g))
 
 
+def kan_forward_tangent(layer: KanLayer, x, tx):
+    """kan_forward on x seeded with the tangent direction tx (the reference's
+    ``T.seed_tangent(x, tx)`` then ``y.tangent``, tensor.py:411-424): returns (y, ty) with
+    ty = (dy/dx) . tx, differentiable in x, tx and the parameters (forward-over-reverse)."""
+    x = as_input(x, layer.coeffs.device)
+    tx = as_input(tx, layer.coeffs.device)
+    if tx.shape != x.shape:
+        raise DimensionError(f"tangent seed shape {tuple(tx.shape)} != {tuple(x.shape)}")
+    y = kan_forward(layer, x)
+    ty = ops.KanJvpFn.apply(x, tx, layer.coeffs, layer.scale, layer.base_weight, layer.G, layer.k,
+                            float(layer.g_min), float(layer.g_max))
+    return y, ty
+
+
+def ukan_forward_tangent(layer: UkanLayer, x, tx, dedup: bool = True):
+    """ukan_forward on x seeded with the tangent tx: (y, ty), one generated table shared by both."""
+    x = as_input(x, layer.scale.device)
+    tx = as_input(tx, layer.scale.device)
+    if x.ndim != 2 or x.shape[1] != layer.d_in:
+        raise DimensionError(f"expected [batch, {layer.d_in}] input, got {tuple(x.shape)}")
+    if tx.shape != x.shape:
+        raise DimensionError(f"tangent seed shape {tuple(tx.shape)} != {tuple(x.shape)}")
+    keys = ops.ukan_build_keys(x.detach(), layer.k, float(layer.delta_g))
+    table = _cg_table(layer, keys)
+    y = ops.UkanSplineFn.apply(x, table, layer.scale, keys.base_row, keys.seg_start, layer.k, float(layer.delta_g))
+    ty = ops.UkanJvpFn.apply(x, tx, table, layer.scale, keys.base_row, keys.seg_start, layer.k,
+                             float(layer.delta_g))
+    return y, ty
+
+
 def cg_coefficients(layer: UkanLayer, f: int, g: int) -> torch.Tensor:
     """Coefficients of one grid group, shape [d_out, K] (layers.py:246-251)."""
     if not (0 <= f < layer.d_in):
@@ -266,6 +302,16 @@ class Model:
     """A stack of layers; spline layers connect directly, 'mlp' inserts SiLU (layers.py:413-435)."""
     kind: str
     layers: list = field(default_factory=list)
+
+    def forward_tangent(self, x, tx):
+        """(f(x), df/dx . tx) through the spline stack (the reference's seed_tangent +
+        Model.forward, tensor.py:411-424, layers.py:420-426)."""
+        if self.kind == "mlp":
+            raise ConfigError("forward_tangent covers spline stacks (kan / ukan)")
+        h, th = x, tx
+        for layer in self.layers:
+            h, th = layer.forward_tangent(h, th)
+        return h, th
 
     def forward(self, x):
         h = x

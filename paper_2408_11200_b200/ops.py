@@ -292,3 +292,80 @@ class UkanSplineFn(torch.autograd.Function):
                                      ptr(dx), ptr(dtable), ptr(ds), B, d_in, d_out, n_u, k, delta_g, ptr(ws),
                                      nbytes, stream_ptr()), "ukan_backward")
         return dx, dtable, ds, None, None, None, None
+
+
+class KanJvpFn(torch.autograd.Function):
+    """Forward tangent ty = (dy/dx) . tx of kan_forward — the tangent channel of basis_features /
+    edge_combine / clamp / silu (layers.py:49-53, 91-104; tensor.py:236-241, 336-337).  Its
+    backward is the reverse pass through that tangent graph (forward-over-reverse, as pinn_loss
+    needs, tasks.py:153-166): dx (tangent share), dtx, dcoeffs, dscale, dbase_weight."""
+
+    @staticmethod
+    def forward(ctx, x, tx, coeffs, scale, base_weight, G: int, k: int, g_min: float, g_max: float):
+        lib = _lib.load()
+        _lib.require_cuda(x, tx, coeffs, scale, base_weight)
+        x, tx = _f32(x), _f32(tx)
+        B, d_in = x.shape
+        d_out = coeffs.shape[2]
+        ty = torch.empty((B, d_out), device=x.device, dtype=torch.float32)
+        check(lib.ukan_kan_jvp_forward(ptr(x), ptr(tx), ptr(coeffs), ptr(scale), ptr(base_weight), ptr(ty), B, d_in,
+                                       d_out, G, k, g_min, g_max, stream_ptr()), "kan_jvp_forward")
+        ctx.save_for_backward(x, tx, coeffs, scale, base_weight)
+        ctx.meta = (G, k, float(g_min), float(g_max))
+        return ty
+
+    @staticmethod
+    def backward(ctx, gt):
+        lib = _lib.load()
+        x, tx, coeffs, scale, bw = ctx.saved_tensors
+        G, k, g_min, g_max = ctx.meta
+        gt = _f32(gt)
+        B, d_in = x.shape
+        d_out = coeffs.shape[2]
+        dx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
+        dtx = torch.empty_like(tx) if ctx.needs_input_grad[1] else None
+        dC = torch.empty_like(coeffs)
+        ds = torch.empty_like(scale)
+        dbw = torch.empty_like(bw) if bw is not None else None
+        check(lib.ukan_kan_jvp_backward(ptr(x), ptr(tx), ptr(coeffs), ptr(scale), ptr(bw), ptr(gt), ptr(dx), ptr(dtx),
+                                        ptr(dC), ptr(ds), ptr(dbw), B, d_in, d_out, G, k, g_min, g_max,
+                                        stream_ptr()), "kan_jvp_backward")
+        return dx, dtx, dC, ds, dbw, None, None, None, None
+
+
+class UkanJvpFn(torch.autograd.Function):
+    """Forward tangent of the UKAN spline over the generated table (u = x/dg - g_id carries
+    tx/dg, layers.py:264; the table itself has no tangent) and its reverse pass: dx (tangent
+    share), dtx, dtable (flows on into the CG backward), dscale."""
+
+    @staticmethod
+    def forward(ctx, x, tx, table, scale, base_row, seg_start, k: int, delta_g: float):
+        lib = _lib.load()
+        _lib.require_cuda(x, tx, table, scale)
+        x, tx = _f32(x), _f32(tx)
+        B, d_in = x.shape
+        d_out = scale.shape[1]
+        ty = torch.empty((B, d_out), device=x.device, dtype=torch.float32)
+        check(lib.ukan_ukan_jvp_forward(ptr(x), ptr(tx), ptr(base_row), ptr(table), ptr(scale), ptr(ty), B, d_in,
+                                        d_out, k, delta_g, stream_ptr()), "ukan_jvp_forward")
+        ctx.save_for_backward(x, tx, table, scale, base_row, seg_start)
+        ctx.meta = (k, float(delta_g))
+        return ty
+
+    @staticmethod
+    def backward(ctx, gt):
+        lib = _lib.load()
+        x, tx, table, scale, base_row, seg_start = ctx.saved_tensors
+        k, delta_g = ctx.meta
+        gt = _f32(gt)
+        B, d_in = x.shape
+        d_out = scale.shape[1]
+        n_u = table.shape[0]
+        dx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
+        dtx = torch.empty_like(tx) if ctx.needs_input_grad[1] else None
+        dtable = torch.empty_like(table)
+        ds = torch.empty_like(scale)
+        check(lib.ukan_ukan_jvp_backward(ptr(x), ptr(tx), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale),
+                                         ptr(gt), ptr(dx), ptr(dtx), ptr(dtable), ptr(ds), B, d_in, d_out, n_u, k,
+                                         delta_g, stream_ptr()), "ukan_jvp_backward")
+        return dx, dtx, dtable, ds, None, None, None, None

@@ -117,6 +117,53 @@ def run_step(name, kind, widths, k, B, seed, loss_kind, layer_kw, lr=1e-2, wd=1e
     print(name, "losses", losses)
 
 
+def run_tangent(name, kind, widths, k, B, seed, layer_kw, xgen):
+    """Forward tangent through a spline stack (F2): x seeded with tx (tensor.py:411-424),
+    L = sum(y * gup) + sum(y.tangent * gt), reference tape backward."""
+    from ukan import tensor as T
+    from ukan.layers import build_model
+    model = build_model(kind, widths, k, seed=seed, **layer_kw)
+    for p in model.parameters().values():
+        p.values[...] = f32(p.values)
+    rng = np.random.default_rng(seed + 1)
+    x = f32(xgen(rng, (B, widths[0])))
+    tx = f32(rng.normal(size=(B, widths[0])))
+    r2 = np.random.default_rng(seed + 2)
+    gup = f32(r2.normal(size=(B, widths[-1])))
+    gt = f32(r2.normal(size=(B, widths[-1])))
+    xp = T.parameter(x.copy())
+    y = model(T.seed_tangent(xp, tx))
+    ty = y.tangent
+    T.backward(T.add(T.sum_all(T.mul(y, T.as_tensor(gup))), T.sum_all(T.mul(ty, T.as_tensor(gt)))))
+    out = dict(kind=kind, widths=np.array(widths), k=k, x=x, tx=tx, g_up=gup, g_tan=gt, y=y.values,
+               ty=ty.values, dx=xp.grad, **{f"kw_{a}": b for a, b in layer_kw.items()})
+    for n, p in model.parameters().items():
+        out[n] = p.values
+        out["d" + n] = p.grad
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "ty", ty.values.shape)
+
+
+def run_pinn(name, kind, k, seed, layer_kw, n_colloc=16):
+    """pinn_loss (tasks.py:153-166) of a [1, 5, 1] stack and its parameter gradients."""
+    from ukan import tensor as T
+    from ukan.layers import build_model
+    from ukan.tasks import PinnProblem, pinn_loss
+    model = build_model(kind, [1, 5, 1], k, seed=seed, **layer_kw)
+    for p in model.parameters().values():
+        p.values[...] = f32(p.values)
+    problem = PinnProblem(1.0, -5.0, 5.0, n_colloc)
+    colloc = f32(problem.sample_collocation(np.random.default_rng(seed + 1)))
+    loss = pinn_loss(model.forward, problem, colloc)
+    T.backward(loss)
+    out = dict(kind=kind, k=k, colloc=colloc, loss=float(loss.values), **{f"kw_{a}": b for a, b in layer_kw.items()})
+    for n, p in model.parameters().items():
+        out[n] = p.values
+        out["d" + n] = p.grad
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "loss", float(loss.values))
+
+
 def main():
     sys.path.insert(0, REF)
     import ukan
@@ -159,6 +206,18 @@ def main():
     run_step("step_kan_ce", "kan", [6, 7, 3], 3, 48, 41, "softmax_cross_entropy",
              dict(g_min=-1.0, g_max=1.0, G=8))
     run_step("step_ukan_mse", "ukan", [3, 5, 2], 3, 32, 42, "mse", dict(delta_g=0.5, d_pe=8, d_femb=8))
+
+    run_tangent("tan_kan", "kan", [4, 3], 3, 20, 51, dict(g_min=-1.0, g_max=1.0, G=7), unif(-1.3, 1.3))
+    run_tangent("tan_kan_base", "kan", [3, 4], 3, 18, 52, dict(g_min=-2.0, g_max=2.0, G=5, base=True),
+                unif(-2.5, 2.5))
+    run_tangent("tan_kan_k1", "kan", [3, 2], 1, 16, 53, dict(g_min=-1.0, g_max=1.5, G=6), unif(-1.2, 1.7))
+    run_tangent("tan_kan_stack", "kan", [2, 5, 3], 3, 24, 54, dict(g_min=-1.0, g_max=1.0, G=6), unif(-1, 1))
+    run_tangent("tan_ukan", "ukan", [3, 2], 3, 20, 55, dict(delta_g=0.8, d_pe=8, d_femb=8),
+                lambda r, s: r.normal(0, 4, s))
+    run_tangent("tan_ukan_stack", "ukan", [2, 4, 2], 2, 16, 56, dict(delta_g=0.5, d_pe=6, d_femb=4),
+                lambda r, s: r.normal(0, 2, s))
+    run_pinn("pinn_kan", "kan", 3, 61, dict(g_min=-5.0, g_max=5.0, G=10))
+    run_pinn("pinn_ukan", "ukan", 3, 62, dict(delta_g=0.5, d_pe=8, d_femb=8))
 
 
 if __name__ == "__main__":

@@ -71,3 +71,30 @@ def test_training_step_oracle_matches_reference(name):
 def test_basis_matrix_eq3():
     M = oracle.basis_matrix(3) * 6
     np.testing.assert_array_equal(M, [[1, 4, 1, 0], [-3, 0, 3, 0], [3, -6, 3, 0], [-1, 3, -3, 1]])
+
+
+def _tangent_single(name):
+    return [n for n in golden_names("tan_") if "stack" not in n]
+
+
+@pytest.mark.parametrize("name", _tangent_single("tan_"))
+def test_tangent_oracle_matches_reference(name):
+    """F2: the forward tangent (x seeded with tx) and the gradients of sum(y gup) + sum(ty gt)
+    through the reference's tangent graph, single layer."""
+    g = load_golden(name)
+    k = int(g["k"])
+    if str(g["kind"]) == "kan":
+        r = oracle.kan_tangent_forward_backward(
+            g["x"], g["tx"], g["layer0.coeffs"], g["layer0.scale"], g["g_up"], g["g_tan"], k=k,
+            g_min=float(g["kw_g_min"]), g_max=float(g["kw_g_max"]), G=int(g["kw_G"]),
+            base_weight=g.get("layer0.base_weight"))
+        pairs = [("dcoeffs", "dlayer0.coeffs"), ("dscale", "dlayer0.scale"), ("dbase_weight", "dlayer0.base_weight")]
+    else:
+        names = ["feature_embedding", "cg_w1", "cg_b1", "cg_w2", "cg_b2", "scale"]
+        p = {n: g["layer0." + n] for n in names}
+        r = oracle.ukan_tangent_forward_backward(g["x"], g["tx"], p, g["g_up"], g["g_tan"], k=k,
+                                                 delta_g=float(g["kw_delta_g"]), d_pe=int(g["kw_d_pe"]))
+        pairs = [("d" + n, "dlayer0." + n) for n in names]
+    for key, ref in [("y", "y"), ("ty", "ty"), ("dx", "dx")] + pairs:
+        if ref in g:
+            np.testing.assert_allclose(r[key], g[ref], rtol=1e-10, atol=1e-12, err_msg=f"{name}.{key}")
