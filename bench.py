@@ -283,6 +283,14 @@ def our_arm(args, rank, world, local_rank):
     else:
         hbm_bytes = 4.0 * (B * d0 + B * d1 + d0 * R * d1 + d0 * d1)
     step_fl = kan_flops(B, d0, d1, k) * 2 + kan_flops(B, d1, d2, k) * 3
+    # DRAM bytes per launch of the dominant kernel group from the committed ncu --set full capture
+    traffic = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            grp = json.load(f).get("layer0.kan_backward" if "backward" in dom else "layer0.kan_forward")
+        traffic = grp["dram_bytes"] if grp else None
+    except (OSError, ValueError, KeyError):
+        traffic = None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         sub = 16
@@ -300,7 +308,9 @@ def our_arm(args, rank, world, local_rank):
                    "global_batch": B * world, "per_gpu_batch": B, "parallelism": f"dp{world}",
                    "l2": f"inputs rotate over {ROTATE} HBM-resident batches ({ROTATE * B * d0 * 4 / 2**20:.0f} MiB > 126 MB L2)"},
         "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
-                     "frac": achieved / dom_peak, "traffic": None,
+                     "frac": achieved / dom_peak, "traffic": traffic,
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+                     "algorithmic_bytes_per_launch": hbm_bytes,
                      "peak_source": "tools/peaks.cu FMA microbenchmark on this pool's B200 (profiles/peaks_r01.json)",
                      "algorithmic_flops_per_launch": dom_fl, "avg_launch_ms": dom_ms},
         "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / (dom_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],

@@ -67,3 +67,33 @@ if os.path.exists(rep):
         json.dump({"source": "ncu --set full --clock-control none --import-source on, inside python bench.py "
                              "(KAN [784,256,10] B=8192 training step), layer-0 kernels", "kernels": res}, f, indent=1)
     print(json.dumps(res, indent=1))
+
+    # per-launch DRAM traffic of the dominant kernel groups (bench.py's roofline.traffic)
+    def _bytes(d, key):
+        v, _, unit = d.get(key, "0 byte").partition(" ")
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit.strip(), 1)
+        return float(v.replace(",", "")) * mult
+
+    def _us(d):
+        v, _, unit = d.get("gpu__time_duration.sum", "0 us").partition(" ")
+        return float(v.replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                                            "msecond": 1e3}.get(unit.strip(), 1.0)
+
+    def _group(names):
+        picked = {}
+        for d in res:
+            for n in names:
+                if n in d["kernel"] and (n not in picked or _us(d) > _us(picked[n])):
+                    picked[n] = d
+        if len(picked) < len(names):
+            return None
+        return {"kernels": [picked[n]["kernel"] for n in names],
+                "dram_bytes": sum(_bytes(picked[n], "dram__bytes_read.sum") + _bytes(picked[n], "dram__bytes_write.sum")
+                                  for n in names)}
+
+    traffic = {"source": f"profiles/ncu_full_{tag}.json (ncu --set full, one launch per kernel, largest of each name)",
+               "layer0.kan_backward": _group(["kan_bwd_tc_prep_kernel", "kan_bwd_tc2_sweep_kernel"]),
+               "layer0.kan_forward": _group(["kan_pack_coeffs_kernel", "kan_fwd_records_kernel", "kan_fwd_tm_kernel"])}
+    with open(os.path.join(out, "traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print(json.dumps(traffic, indent=1))
