@@ -292,9 +292,9 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, kq = lane & 3;
   const int fl = warp / WPF, h = warp % WPF;
-  const int i0 = blockIdx.x * FPB;
+  const int i0 = blockIdx.y * FPB;  // output tiles fastest: the CTAs sharing a feature group's records run together
   const int i = i0 + fl;
-  const int o0 = blockIdx.y * OPB;
+  const int o0 = blockIdx.x * OPB;
   const int z = blockIdx.z;
   const int n_lo = z * cps, n_hi = min(nch, n_lo + cps);
   const int R = G + 3;
@@ -532,7 +532,7 @@ static int tc2_launch(const float* C, const float* scale, const float* gy, float
                       cudaStream_t st) {
   auto kern = kan_bwd_tc2_sweep_kernel<RB, NT, FPB, WPF>;
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  dim3 gridd((d_in + FPB - 1) / FPB, (d_out + 8 * NT - 1) / (8 * NT), p.S);
+  dim3 gridd((d_out + 8 * NT - 1) / (8 * NT), (d_in + FPB - 1) / FPB, p.S);
   kern<<<gridd, FPB * WPF * 32, p.smem, st>>>(recs, C, scale, gy, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
                                    p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
