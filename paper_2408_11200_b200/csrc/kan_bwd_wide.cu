@@ -21,8 +21,10 @@
 // Deterministic: fixed chunk order, cell-then-sample order inside a chunk, fixed reductions.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "rowmap.cuh"
 
 namespace ukan {
 
@@ -178,21 +180,26 @@ kan_bwd_wide_sweep_kernel(const unsigned char* __restrict__ recs, const float* _
       }
       __syncwarp();
       const int ns = min(32, hi - p0);
-      float gv[32];
+      const float* gyo = gy + (live ? o : 0);
+      for (int q0 = 0; q0 < ns; q0 += 16) {
+        const int nq = min(16, ns - q0);
+        unsigned gv[16];  // 16 independent gathers in flight
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
-        gv[q] = (q < ns && live) ? __ldg(gy + (size_t)bb[q] * d_out + o) : 0.f;
+        for (int q = 0; q < 16; ++q)
+          gv[q] = (q < nq && live) ? __float_as_uint(__ldg(gyo + (size_t)bb[q0 + q] * d_out)) : 0u;
+        __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        if (q < ns) {
-          const int cell = cb[q];
-          if (cell != cur) {
-            flush();
-            cur = cell;
+        for (int q = 0; q < 16; ++q) {
+          if (q < nq) {
+            const int cell = cb[q0 + q];
+            if (cell != cur) {
+              flush();
+              cur = cell;
+            }
+            const double g = (double)__uint_as_float(gv[q]);
+#pragma unroll
+            for (int j = 0; j < K; ++j) acc[j] = fma(wb[q0 + q][j], g, acc[j]);
           }
-          const double g = (double)gv[q];
-#pragma unroll
-          for (int j = 0; j < K; ++j) acc[j] = fma(wb[q][j], g, acc[j]);
         }
       }
       __syncwarp();
@@ -298,5 +305,347 @@ int kan_bwd_wide_run(const float* x, const float* C, const float* scale, const f
                                    cudaStream_t);
 UKAN_WIDE_INST(1) UKAN_WIDE_INST(2) UKAN_WIDE_INST(3) UKAN_WIDE_INST(4) UKAN_WIDE_INST(5) UKAN_WIDE_INST(6)
 UKAN_WIDE_INST(7) UKAN_WIDE_INST(8) UKAN_WIDE_INST(9) UKAN_WIDE_INST(10) UKAN_WIDE_INST(11)
+
+// ---------------------------------------------------------------------------------------
+// Segmented variant for data-dependent per-feature row segments (UKAN's generated table,
+// layers.py:254-291: feature f owns rows [seg_start[f]*K, seg_start[f+1]*K) of the [n_u*K, d_out]
+// table, a window is base_row + 0..k).  Same records (256-sample chunks sorted by local row),
+// but the tiles are per-feature 32-row tiles enumerated by a prefix over the segment lengths,
+// and a CTA of W warps (32*W outputs) shares one tile's sample staging: the chunk bounds are
+// found by counting keys (no per-tile index), basis weights evaluated once per CTA.
+template <bool UKAN>
+__global__ void __launch_bounds__(256)
+seg_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ recs, int B, int d_in, int nch,
+                RowMap rm) {
+  __shared__ float xs[kWdBC][9];
+  __shared__ __align__(16) int keys[8][kWdBC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * 8, n = blockIdx.y;
+  const int b0 = n * kWdBC;
+  const int nb = min(kWdBC, B - b0);
+  for (int t = threadIdx.x; t < kWdBC * 8; t += blockDim.x) {
+    const int s = t / 8, f = t % 8;
+    xs[s][f] = (s < nb && i0 + f < d_in) ? x[(size_t)(b0 + s) * d_in + i0 + f] : 0.f;
+  }
+  __syncthreads();
+  const int i = i0 + warp;
+  if (i >= d_in) return;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  unsigned char* rec = recs + ((size_t)i * nch + n) * (kWdBC * 12);
+  int* ent = reinterpret_cast<int*>(rec);
+  double* uu = reinterpret_cast<double*>(rec + kWdBC * 4);
+  constexpr int PER = kWdBC / 32;
+  int key[PER];
+  double us[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int s = q * 32 + lane;
+    int local = kWdBadCell;
+    double u = 0.0;
+    if (s < nb) {
+      int row;
+      bool mask;
+      if (locate_row<UKAN>(rm, xs[s][warp], (int64_t)(b0 + s), i, d_in, row, u, mask)) local = row - row0;
+    }
+    key[q] = (local << 8) | s;
+    us[q] = u;
+    keys[warp][s] = key[q];
+  }
+  __syncwarp();
+  int rank[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) rank[q] = 0;
+  const int4* k4 = reinterpret_cast<const int4*>(keys[warp]);
+  for (int m = 0; m < kWdBC / 4; ++m) {
+    const int4 v = k4[m];
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      rank[q] += (v.x < key[q]) + (v.y < key[q]) + (v.z < key[q]) + (v.w < key[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    ent[rank[q]] = key[q];
+    uu[rank[q]] = us[q];
+  }
+}
+
+// tile_start[f] = sum_{f' < f} ceil(rows(f') / 32)   (one warp, 32 features per step)
+template <bool UKAN>
+__global__ void seg_tiles_kernel(RowMap rm, int d_in, int* __restrict__ tile_start) {
+  const int lane = threadIdx.x;
+  int carry = 0;
+  for (int f0 = 0; f0 <= d_in; f0 += 32) {
+    const int f = f0 + lane;
+    int v = 0;
+    if (f < d_in) {
+      int row0, nrows;
+      feature_rows<UKAN>(rm, f, row0, nrows);
+      v = (nrows + kWdRT - 1) / kWdRT;
+    }
+    int inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += t;
+    }
+    if (f <= d_in) tile_start[f] = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+constexpr int kSegSB = 256;     // samples staged per batch
+constexpr int kSegMaxCh = 512;  // chunks (B <= 131072)
+constexpr int kSegGB = 16;      // samples per g stage (cp.async double buffer)
+
+template <int K>
+__host__ __device__ constexpr size_t seg_smem_bytes(int W) {
+  return sizeof(double) * ((size_t)W * kWdRT * 32 + (size_t)kSegSB * K) + sizeof(float) * 2 * kSegGB * 32 * W +
+         sizeof(int) * (2 * kSegSB + 3 * kSegMaxCh + 8);
+}
+
+template <int K, bool UKAN>
+__global__ void __launch_bounds__(256)
+seg_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ T, const float* __restrict__ scale,
+                 const float* __restrict__ gy, float* __restrict__ dT, double* __restrict__ part,
+                 const int* __restrict__ tile_start, int d_in, int d_out, int nch, int n_og, RowMap rm,
+                 Basis<K> bas) {
+  extern __shared__ __align__(16) double ssm[];
+  const int W = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double (*A)[32] = reinterpret_cast<double (*)[32]>(ssm + (size_t)warp * kWdRT * 32);
+  double (*wb)[K] = reinterpret_cast<double (*)[K]>(ssm + (size_t)W * kWdRT * 32);
+  int* cb = reinterpret_cast<int*>(ssm + (size_t)W * kWdRT * 32 + (size_t)kSegSB * K);
+  int* bb = cb + kSegSB;
+  int* c_lo = bb + kSegSB;       // [nch] first sorted position of the tile's samples in chunk c
+  int* c_off = c_lo + kSegMaxCh;  // [nch + 1] exclusive prefix of the per-chunk counts
+  float* gs = reinterpret_cast<float*>(c_off + 2 * kSegMaxCh + 8);  // [2][kSegGB][32*W] g rows of a stage
+  const int64_t blk = blockIdx.x;
+  const int og = (int)(blk % n_og);
+  const int tt = (int)(blk / n_og);
+  if (tt >= tile_start[d_in]) return;
+  int lo_f = 0, hi_f = d_in - 1;  // feature: largest f with tile_start[f] <= tt
+  while (lo_f < hi_f) {
+    const int mid = (lo_f + hi_f + 1) >> 1;
+    if (tile_start[mid] <= tt) lo_f = mid;
+    else hi_f = mid - 1;
+  }
+  const int i = lo_f;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  const int r0 = (tt - tile_start[i]) * kWdRT;
+  const int lo_key = max(0, r0 - (K - 1)) << 8, hi_key = (r0 + kWdRT) << 8;
+  const int o = (og * W + warp) * 32 + lane;
+  const bool live = o < d_out;
+  // 1. the tile's sample range in every sorted chunk (warp per chunk, keys counted lane-parallel)
+  for (int c = warp; c < nch; c += W) {
+    const int4* e4 = reinterpret_cast<const int4*>(recs + ((size_t)i * nch + c) * (kWdBC * 12)) + lane * 2;
+    const int4 ka = __ldg(e4), kb = __ldg(e4 + 1);
+    int nlo = (ka.x < lo_key) + (ka.y < lo_key) + (ka.z < lo_key) + (ka.w < lo_key) + (kb.x < lo_key) +
+              (kb.y < lo_key) + (kb.z < lo_key) + (kb.w < lo_key);
+    int nhi = (ka.x < hi_key) + (ka.y < hi_key) + (ka.z < hi_key) + (ka.w < hi_key) + (kb.x < hi_key) +
+              (kb.y < hi_key) + (kb.z < hi_key) + (kb.w < hi_key);
+    nlo = __reduce_add_sync(0xffffffffu, nlo);
+    nhi = __reduce_add_sync(0xffffffffu, nhi);
+    if (lane == 0) {
+      c_lo[c] = nlo;
+      c_off[c + 1] = nhi - nlo;
+    }
+  }
+#pragma unroll 4
+  for (int r = 0; r < kWdRT; ++r) A[r][lane] = 0.0;
+  __syncthreads();
+  if (warp == 0) {  // inclusive scan of the counts (chunk order = sample order)
+    int carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      int v = c < nch ? c_off[c + 1] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += t;
+      }
+      if (c < nch) c_off[c + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) c_off[0] = 0;
+  }
+  __syncthreads();
+  const int N = c_off[nch];
+  double acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = 0.0;
+  int cur = INT_MIN;
+  auto flush = [&]() {
+    if (cur != INT_MIN) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int r = cur + j - r0;
+        if (r >= 0 && r < kWdRT) A[r][lane] += acc[j];
+        acc[j] = 0.0;
+      }
+    }
+  };
+  // 2. stage the tile's samples (chunk order, sorted inside a chunk) in batches, then sweep them
+  for (int s0 = 0; s0 < N; s0 += kSegSB) {
+    const int nb = min(kSegSB, N - s0);
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+      const int gq = s0 + q;
+      int lo = 0, hi = nch - 1;  // chunk: largest c with c_off[c] <= gq
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (c_off[mid] <= gq) lo = mid;
+        else hi = mid - 1;
+      }
+      const int c = lo;
+      const int p = c_lo[c] + (gq - c_off[c]);
+      const unsigned char* rec = recs + ((size_t)i * nch + c) * (kWdBC * 12);
+      const int key = __ldg(reinterpret_cast<const int*>(rec) + p);
+      double w[K];
+      basis_weights<K>(bas, __ldg(reinterpret_cast<const double*>(rec + kWdBC * 4) + p), w);
+#pragma unroll
+      for (int j = 0; j < K; ++j) wb[q][j] = w[j];
+      cb[q] = key >> 8;
+      bb[q] = (c * kWdBC + (key & 255)) * d_out;  // element offset of the sample's g row
+    }
+    __syncthreads();
+    // g rows of the staged samples: coalesced cp.async of [kSegGB samples][32*W outputs], double
+    // buffered so the next stage is in flight while this one is swept
+    const int OW = 32 * W, o_base = og * OW;
+    const int n_st = (nb + kSegGB - 1) / kSegGB;
+    auto stage_g = [&](int stg) {
+      float* dst = gs + (size_t)(stg & 1) * kSegGB * OW;
+      const int q0 = stg * kSegGB;
+      const int nq = min(kSegGB, nb - q0);
+      if ((d_out & 3) == 0) {
+        const int v4 = OW / 4;
+        for (int t = threadIdx.x; t < kSegGB * v4; t += blockDim.x) {
+          const int q = t / v4, oc = (t % v4) * 4;
+          const int oo = o_base + oc;
+          const int bytes = q < nq ? max(0, min(4, d_out - oo)) * 4 : 0;
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + q * OW + oc);
+          const float* src = bytes ? gy + (size_t)(unsigned)bb[q0 + q] + oo : gy;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+        }
+      } else {
+        for (int t = threadIdx.x; t < kSegGB * OW; t += blockDim.x) {
+          const int q = t / OW, oc = t % OW;
+          const int oo = o_base + oc;
+          const bool ok = q < nq && oo < d_out;
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + q * OW + oc);
+          const float* src = ok ? gy + (size_t)(unsigned)bb[q0 + q] + oo : gy;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 4 : 0));
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    stage_g(0);
+    for (int stg = 0; stg < n_st; ++stg) {
+      if (stg + 1 < n_st) {
+        stage_g(stg + 1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      __syncthreads();
+      const float* gq = gs + (size_t)(stg & 1) * kSegGB * OW + warp * 32 + lane;
+      const int q0 = stg * kSegGB;
+      const int nq = min(kSegGB, nb - q0);
+      for (int q = 0; q < nq; ++q) {
+        const int cell = cb[q0 + q];
+        if (cell != cur) {
+          if (cell > cur && cell - cur < K && cur != INT_MIN) {
+            // sorted run advances: slide the K-row register window, retiring one row per step
+            do {
+              const int r = cur - r0;
+              if (r >= 0 && r < kWdRT) A[r][lane] += acc[0];
+#pragma unroll
+              for (int j = 0; j + 1 < K; ++j) acc[j] = acc[j + 1];
+              acc[K - 1] = 0.0;
+            } while (++cur < cell);
+          } else {
+            flush();
+            cur = cell;
+          }
+        }
+        const double g = (double)gq[q * OW];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fma(wb[q0 + q][j], g, acc[j]);
+      }
+      __syncthreads();  // stage buffer (stg & 1) is refilled by the next iteration's stage_g
+    }
+  }
+  flush();
+  __syncwarp();
+  if (live) {
+    const double sc = (double)__ldg(scale + (size_t)i * d_out + o);
+    double prod = 0.0;
+    for (int r = 0; r < kWdRT && r0 + r < nrows; ++r) {
+      const double a = A[r][lane];
+      const size_t ci = (size_t)(row0 + r0 + r) * d_out + o;
+      dT[ci] = (float)(sc * a);
+      prod = fma((double)__ldg(T + ci), a, prod);
+    }
+    part[(size_t)tt * d_out + o] = prod;
+  }
+}
+
+// dscale[f,o] = sum over the feature's tiles (fixed order)
+__global__ void seg_reduce_kernel(const double* __restrict__ part, const int* __restrict__ tile_start,
+                                  float* __restrict__ dscale, int d_in, int d_out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)d_in * d_out) return;
+  const int i = (int)(e / d_out), o = (int)(e % d_out);
+  double a = 0.0;
+  for (int t = tile_start[i]; t < tile_start[i + 1]; ++t) a += part[(size_t)t * d_out + o];
+  dscale[e] = (float)a;
+}
+
+bool seg_supported(int64_t B) { return (B + kWdBC - 1) / kWdBC <= kSegMaxCh; }
+bool seg_supported(int64_t B, int64_t d_out) { return seg_supported(B) && B * d_out < ((int64_t)1 << 31); }
+
+int64_t seg_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t total_rows) {
+  const int64_t nch = (B + kWdBC - 1) / kWdBC;
+  const int64_t rec = ((d_in * nch * kWdBC * 12 + 255) / 256) * 256;
+  const int64_t ts = ((4 * (d_in + 1) + 255) / 256) * 256;
+  const int64_t tiles = (total_rows + kWdRT - 1) / kWdRT + d_in;
+  return rec + ts + (int64_t)sizeof(double) * tiles * d_out;
+}
+
+template <int K, bool UKAN>
+int seg_table_grad(const float* x, const float* T, const float* scale, const float* gy, float* dT, float* dscale,
+                   void* ws, int64_t ws_bytes, int B, int d_in, int d_out, int64_t total_rows, const RowMap& rm,
+                   cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < seg_workspace(B, d_in, d_out, total_rows)) return UKAN_E_WORKSPACE;
+  const int nch = (B + kWdBC - 1) / kWdBC;
+  unsigned char* recs = reinterpret_cast<unsigned char*>(ws);
+  const int64_t rec = (((int64_t)d_in * nch * kWdBC * 12 + 255) / 256) * 256;
+  int* tile_start = reinterpret_cast<int*>(recs + rec);
+  double* part = reinterpret_cast<double*>(recs + rec + ((4 * ((int64_t)d_in + 1) + 255) / 256) * 256);
+  const int64_t tiles = (total_rows + kWdRT - 1) / kWdRT + d_in;
+  seg_prep_kernel<UKAN><<<dim3((d_in + 7) / 8, nch), 256, 0, st>>>(x, recs, B, d_in, nch, rm);
+  UKAN_LAUNCH_CHECK();
+  seg_tiles_kernel<UKAN><<<1, 32, 0, st>>>(rm, d_in, tile_start);
+  UKAN_LAUNCH_CHECK();
+  const int n_os = (d_out + 31) / 32;
+  const int W = std::min(8, n_os);
+  const int n_og = (n_os + W - 1) / W;
+  const size_t smem = seg_smem_bytes<K>(W);
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(seg_sweep_kernel<K, UKAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  seg_sweep_kernel<K, UKAN><<<(unsigned)(tiles * n_og), 32 * W, smem, st>>>(recs, T, scale, gy, dT, part, tile_start,
+                                                                           d_in, d_out, nch, n_og, rm,
+                                                                           make_basis<K>(K - 1));
+  UKAN_LAUNCH_CHECK();
+  const int64_t n = (int64_t)d_in * d_out;
+  seg_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, tile_start, dscale, d_in, d_out);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+#define UKAN_SEG_INST(K)                                                                                        \
+  template int seg_table_grad<K, true>(const float*, const float*, const float*, const float*, float*, float*, \
+                                       void*, int64_t, int, int, int, int64_t, const RowMap&, cudaStream_t);
+UKAN_SEG_INST(1) UKAN_SEG_INST(2) UKAN_SEG_INST(3) UKAN_SEG_INST(4) UKAN_SEG_INST(5) UKAN_SEG_INST(6)
+UKAN_SEG_INST(7) UKAN_SEG_INST(8) UKAN_SEG_INST(9) UKAN_SEG_INST(10) UKAN_SEG_INST(11)
 
 }  // namespace ukan

@@ -382,7 +382,9 @@ spline_dx_kernel(const float* __restrict__ x, const float* __restrict__ T,
   const int lane = threadIdx.x % 32;
   const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (pair >= (int64_t)B * d_in) return;
-  const int b = (int)(pair / d_in), i = (int)(pair % d_in);
+  // feature-major: the warps resident at any time share a few features' table rows, so the
+  // gathers hit L2 even when the whole table (UKAN: n_u*K rows) is far larger than L2
+  const int i = (int)(pair / B), b = (int)(pair % B);
   const float xv = x[(size_t)b * d_in + i];
   int row;
   double u;
@@ -506,6 +508,12 @@ template <int K>
 int kan_bwd_wide_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                      float* dbw, void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int R,
                      const KanGrid& grid, const WidePlan& p, cudaStream_t st);
+int64_t seg_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t total_rows);
+bool seg_supported(int64_t B, int64_t d_out);
+template <int K, bool UKAN>
+int seg_table_grad(const float* x, const float* T, const float* scale, const float* gy, float* dT, float* dscale,
+                   void* ws, int64_t ws_bytes, int B, int d_in, int d_out, int64_t total_rows, const RowMap& rm,
+                   cudaStream_t st);
 template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
@@ -851,10 +859,16 @@ extern "C" int ukan_ukan_forward(const float* x, const int32_t* base_row, const 
   return UKAN_OK;
 }
 
+// Sorted-chunk segmented sweep (kan_bwd_wide.cu) when the per-feature local row index fits the
+// 23-bit key field (at most 2*B*K rows per feature); the global fp64 accumulator otherwise.
+static bool ukan_seg_ok(int64_t B, int64_t d_out, int k) {
+  return 2 * B * (k + 1) < ((int64_t)1 << 23) - 64 && seg_supported(B, d_out);
+}
+
 extern "C" int64_t ukan_ukan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
                                                      int64_t n_u, int k) {
-  (void)B;
-  (void)d_in;
+  if (ukan_seg_ok(B, d_out, k) && getenv("UKAN_UKAN_BWD") == nullptr)
+    return seg_workspace(B, d_in, d_out, n_u * (k + 1));
   return (int64_t)sizeof(double) * n_u * (k + 1) * d_out;
 }
 
@@ -877,6 +891,21 @@ extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
   rm.seg_start = seg_start;
   rm.K = k + 1;
   cudaStream_t st = (cudaStream_t)stream;
+  if (B > 0 && ukan_seg_ok(B, d_out, k) && getenv("UKAN_UKAN_BWD") == nullptr) {
+    UKAN_DISPATCH_K(k, {
+      int rc = seg_table_grad<K, true>(x, table, scale, gy, dtable, dscale, workspace, workspace_bytes, (int)B,
+                                       (int)d_in, (int)d_out, n_u * (k + 1), rm, st);
+      if (rc) return rc;
+      if (dx) {
+        const int64_t pairs = B * d_in;
+        spline_dx_kernel<K, true><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, table, scale, nullptr, gy, dx,
+                                                                               (int)B, (int)d_in, (int)d_out, rm,
+                                                                               make_basis<K>(K - 1));
+        UKAN_LAUNCH_CHECK();
+      }
+      return UKAN_OK;
+    });
+  }
   // the fp64 accumulator lives in the global workspace (feature segments are data dependent)
   UKAN_DISPATCH_K(k, return launch_bwd<K, true>(x, table, scale, nullptr, gy, dx, dtable, dscale, nullptr, (double*)workspace, (int)B, (int)d_in, (int)d_out, 1 << 30, rm, st););
   return UKAN_OK;

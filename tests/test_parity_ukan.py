@@ -156,3 +156,20 @@ def test_keys_at_scale_heavy_tails():
     f = np.broadcast_to(np.arange(1024)[None, :], x.shape)
     want_keys = np.unique(np.concatenate([(group * 1024 + f).ravel(), ((group + 1) * 1024 + f).ravel()]))
     check_keys(x, 3, 0.5, g_id, want_keys)
+
+
+@pytest.mark.parametrize("d_out,sigma", [(40, 2.0), (37, 30.0)])
+def test_ukan_segmented_sweep_multi_chunk(d_out, sigma):
+    """B = 1000 spans four 256-sample chunks (partial last one).  sigma = 2 packs every sample
+    of a feature into one 32-row tile (> 256 staged samples -> several batches); sigma = 30
+    spreads them over many tiles; d_out = 37 takes the 4-byte staging path."""
+    layer, x, gup = random_case(1000, 3, d_out, 3, 1.0, 8, 8, seed=40 + d_out, sigma=sigma)
+    check_against_oracle(layer, x, gup)
+    for p in layer.parameters().values():
+        p.grad = None
+    a = run(layer, x, gup)
+    for p in layer.parameters().values():
+        p.grad = None
+    b = run(layer, x, gup)
+    for key in a:
+        np.testing.assert_array_equal(a[key], b[key])
