@@ -63,7 +63,10 @@ def test_workspace_queries():
     recb = 256 * 12 + (n_rt + 1 + 3) // 4 * 4 * 4
     assert lib.ukan_kan_backward_workspace_size(4096, 32, 32, 4096, 3) == 32 * 16 * recb + 8 * 32 * n_rt * 32
     assert lib.ukan_ukan_keys_workspace_size(100, 10, 1000) > 2 * 1000 * 8
-    assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == 8 * 10 * 4 * 3
+    # segmented sweep: sorted chunk records (256 x 12 B per feature and chunk) + tile starts + fp64
+    # dscale partials per 32-row tile (n_u*K rows, plus one partial tile per feature)
+    rec, ts, tiles = 4 * 1 * 256 * 12, 256, (10 * 4 + 31) // 32 + 4
+    assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == rec + ts + 8 * tiles * 3
 
 
 def test_argument_errors_without_gpu():
