@@ -238,6 +238,12 @@ int ukan_adam_step(float* p, const float* g, float* m, float* v, int64_t n, doub
                    const double* guard, void* stream);
 
 /* SGD step p -= lr*g (optim.py:18-21), same guard semantics. */
+/* Graph-replayable Adam (for a step captured as a CUDA graph): increments the device step
+ * counter *t, computes the bias corrections 1 - beta^t into bc[2] (device), reads the learning
+ * rate from *lr (device) and updates as ukan_adam_step.  All of t, bc, lr are device pointers. */
+int ukan_adam_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const double* lr,
+                       double beta1, double beta2, double eps, double weight_decay, int64_t* t,
+                       double* bc, const double* guard, void* stream);
 int ukan_sgd_step(float* p, const float* g, int64_t n, double lr, const double* guard,
                   void* stream);
 

@@ -51,6 +51,7 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_ukan_jvp_forward": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _INT, _F64, _P]),
     "ukan_ukan_jvp_backward": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT,
                                       _F64, _P]),
+    "ukan_adam_step_dev": (_INT, [_P, _P, _P, _P, _I64, _P, _F64, _F64, _F64, _F64, _P, _P, _P, _P]),
     "ukan_kan_locate": (_INT, [_P, _P, _P, _I64, _I64, _I64, _F64, _F64, _P]),
     "ukan_ukan_keys_workspace_size": (_I64, [_I64, _I64, _I64]),
     "ukan_ukan_build_keys": (_INT, [_P, _I64, _I64, _INT, _F64, _P, _P, _P, _P, _I64, _P, _I64, _P, _P,

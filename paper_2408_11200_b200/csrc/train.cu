@@ -73,6 +73,33 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
   p[t] = (float)(pv - lr * (mv / bc1) / (sqrt(vv / bc2) + eps));
 }
 
+// Graph-replayable Adam: the step counter, learning rate and bias corrections live on the device
+// (a captured CUDA graph replays the same launch parameters every step).
+__global__ void adam_count_kernel(int64_t* __restrict__ t, double b1, double b2, double* __restrict__ bc) {
+  const int64_t tt = t[0] + 1;
+  t[0] = tt;
+  bc[0] = 1.0 - pow(b1, (double)tt);  // optim.py:38-39
+  bc[1] = 1.0 - pow(b2, (double)tt);
+}
+
+__global__ void adam_dev_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                float* __restrict__ v, int64_t n, const double* __restrict__ lr_dev, double b1,
+                                double b2, double eps, double wd, const double* __restrict__ bc,
+                                const double* __restrict__ guard) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (guard && !isfinite(*guard)) return;
+  const double lr = *lr_dev, bc1 = bc[0], bc2 = bc[1];
+  const double pv = (double)p[t];
+  double gv = (double)g[t];
+  if (wd != 0.0) gv = gv + wd * pv;  // coupled L2 (optim.py:42-43)
+  const double mv = b1 * (double)m[t] + (1.0 - b1) * gv;
+  const double vv = b2 * (double)v[t] + (1.0 - b2) * gv * gv;
+  m[t] = (float)mv;
+  v[t] = (float)vv;
+  p[t] = (float)(pv - lr * (mv / bc1) / (sqrt(vv / bc2) + eps));
+}
+
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, double lr,
                            const double* __restrict__ guard) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,6 +153,19 @@ extern "C" int ukan_adam_step(float* p, const float* g, float* m, float* v, int6
   const double bc2 = 1.0 - pow(beta2, (double)t);
   adam_kernel<<<nblk(n, 256), 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, lr, beta1, beta2, eps,
                                                               weight_decay, bc1, bc2, guard);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+extern "C" int ukan_adam_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const double* lr,
+                                  double beta1, double beta2, double eps, double weight_decay, int64_t* t,
+                                  double* bc, const double* guard, void* stream) {
+  if (n < 0 || !p || !g || !m || !v || !lr || !t || !bc) return UKAN_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  adam_count_kernel<<<1, 1, 0, st>>>(t, beta1, beta2, bc);
+  UKAN_LAUNCH_CHECK();
+  if (n == 0) return UKAN_OK;
+  adam_dev_kernel<<<nblk(n, 256), 256, 0, st>>>(p, g, m, v, n, lr, beta1, beta2, eps, weight_decay, bc, guard);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }

@@ -110,6 +110,7 @@ class SplineTrainer:
         self.device = dev
         self.kernel_launches = 0
         self.timers = None  # optional {name: [(start_event, end_event), ...]} (bench.py)
+        self._dev_state = None  # (step counter, lr, bias corrections) on the device once captured
 
     def _mark(self, name):
         """Record a CUDA event pair around one launch when timing is enabled."""
@@ -253,7 +254,13 @@ class SplineTrainer:
         self.t += 1
         lr = self.lr if lr is None else lr
         n = self.flat.data.numel()
-        if self.optimizer == "adam":
+        if self.optimizer == "adam" and self._dev_state is not None:  # graph-replayable form
+            t_dev, lr_dev, bc = self._dev_state
+            check(self.lib.ukan_adam_step_dev(ptr(self.flat.data), ptr(self.flat.grad), ptr(self.m), ptr(self.v), n,
+                                              ptr(lr_dev), self.beta1, self.beta2, self.eps, self.wd, ptr(t_dev),
+                                              ptr(bc), ptr(loss), st), "adam_dev")
+            self.kernel_launches += 1
+        elif self.optimizer == "adam":
             check(self.lib.ukan_adam_step(ptr(self.flat.data), ptr(self.flat.grad), ptr(self.m), ptr(self.v), n, lr,
                                           self.beta1, self.beta2, self.eps, self.wd, self.t, ptr(loss), st), "adam")
         else:
@@ -261,11 +268,136 @@ class SplineTrainer:
         self.kernel_launches += 1
         return loss
 
+    def capture(self, x: torch.Tensor, target: torch.Tensor) -> "CapturedStep":
+        """Capture one training step on fixed-shape buffers as a CUDA graph (single process).
+        Run at least one eager ``step`` first (lazy buffers); see ``CapturedStep``."""
+        return CapturedStep(self, x, target)
+
     def read_loss(self, loss: torch.Tensor) -> float:
         """Host read of the step's loss; raises DivergedError / IndexError like the reference."""
-        v = float(loss.item())
-        if int(self._err.item()):
+        # one stream sync for both reads (loss 8 B + NaN flag 4 B into pinned host memory)
+        if getattr(self, "_host_rd", None) is None:
+            self._host_rd = (torch.empty(1, dtype=torch.float64).pin_memory(),
+                             torch.empty(1, dtype=torch.int32).pin_memory())
+        hl, he = self._host_rd
+        hl.copy_(loss.reshape(1), non_blocking=True)
+        err = getattr(self, "_err", None)
+        if err is not None:
+            he.copy_(err, non_blocking=True)
+        else:
+            he.zero_()
+        torch.cuda.current_stream(self.device).synchronize()
+        v = float(hl[0])
+        if int(he[0]):
             raise IndexError("non-finite (NaN) input to a bounded-grid KAN layer")
         if not math.isfinite(v):
             raise DivergedError(f"non-finite loss {v}")
         return v
+
+class CapturedStep:
+    """A ``SplineTrainer.step`` recorded once as a CUDA graph and replayed per batch: the whole
+    step (forward, loss, backward, Adam) costs one graph launch on the host, so a loop that reads
+    the loss every step (the reference's train loop, train.py:152-165) no longer exposes the
+    per-kernel host overhead.  Inputs go into the static buffers ``x`` / ``target``; the Adam
+    step counter, learning rate and bias corrections live on the device (``ukan_adam_step_dev``).
+    Capture itself runs no step.  Single process only (NCCL collectives are not captured)."""
+
+    def __init__(self, trainer: "SplineTrainer", x: torch.Tensor, target: torch.Tensor):
+        if trainer.sync.enabled:
+            raise ConfigError("graph capture covers single-process training")
+        if trainer.model.kind != "kan":  # UKAN's key count is data dependent (one host sync per step)
+            raise ConfigError("graph capture covers KAN stacks (fixed shapes)")
+        dev = trainer.device
+        self.trainer = trainer
+        self.x = x.detach().clone()
+        self.target = target.detach().clone()
+        trainer._dev_state = (torch.tensor([trainer.t], dtype=torch.int64, device=dev),
+                              torch.tensor([trainer.lr], dtype=torch.float64, device=dev),
+                              torch.zeros(2, dtype=torch.float64, device=dev))
+        timers, trainer.timers = trainer.timers, None
+        t_host = trainer.t
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss = trainer.step(self.x, self.target)
+        trainer.t = t_host  # capture executed nothing; the device counter advances on replay
+        trainer.timers = timers
+
+    def replay(self, x: torch.Tensor | None = None, target: torch.Tensor | None = None) -> torch.Tensor:
+        """Copy (x, target) into the static buffers (stream-ordered) and run the step; returns the
+        device loss (read it with ``trainer.read_loss``)."""
+        if x is not None:
+            self.x.copy_(x, non_blocking=True)
+        if target is not None:
+            self.target.copy_(target, non_blocking=True)
+        self.graph.replay()
+        return self.loss
+
+    def set_lr(self, lr: float) -> None:
+        self.trainer._dev_state[1].fill_(lr)
+
+    def sync_step_count(self) -> int:
+        """Copy the device step counter back to the trainer (host read)."""
+        self.trainer.t = int(self.trainer._dev_state[0].item())
+        return self.trainer.t
+
+
+class DevicePrefetcher:
+    """Host -> device input pipeline for the training loop: while step s runs on the compute
+    stream, batch s+1 is copied from pinned host memory on a side stream (the reference loads
+    its batches on the host, train.py:152-165; here the copy overlaps the previous step).
+
+    ``host_batches`` yields tuples of (pinned) CPU tensors; iteration yields the same tuples on
+    ``device``.  Every batch is still copied host -> device once per step.  Two device buffer
+    sets are reused round-robin (no allocation per step); a buffer is refilled only after the
+    compute stream has passed the step that read it.  A yielded batch is valid until the
+    iteration after next."""
+
+    def __init__(self, host_batches, device):
+        self._it = iter(host_batches)
+        self._dev = torch.device(device)
+        self._side = torch.cuda.Stream(device=self._dev)
+        self._bufs = [None, None]
+        self._free = [None, None]   # compute-stream event: buffer k no longer read
+        self._ready = [None, None]  # side-stream event: buffer k filled
+        self._k = 0                 # buffer of the next batch to hand out
+        self._have = self._load(0)
+
+    def _load(self, k):
+        try:
+            batch = next(self._it)
+        except StopIteration:
+            return False
+        buf = self._bufs[k]
+        if buf is None or len(buf) != len(batch) or any(b.shape != t.shape or b.dtype != t.dtype
+                                                        for b, t in zip(buf, batch)):
+            buf = tuple(torch.empty(t.shape, dtype=t.dtype, device=self._dev) for t in batch)
+            self._bufs[k] = buf
+        with torch.cuda.stream(self._side):
+            if self._free[k] is not None:
+                self._side.wait_event(self._free[k])
+            for b, t in zip(buf, batch):
+                b.copy_(t, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._side)
+            self._ready[k] = ev
+        return True
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        if not self._have:
+            raise StopIteration
+        cur = torch.cuda.current_stream(self._dev)
+        k = self._k
+        prev = k ^ 1
+        if self._bufs[prev] is not None:  # the previous batch's step is enqueued: its buffer frees after it
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._free[prev] = ev
+        cur.wait_event(self._ready[k])
+        batch = self._bufs[k]
+        self._have = self._load(prev)
+        self._k = prev
+        return batch

@@ -49,3 +49,49 @@ def test_diverged_loss_skips_update_and_raises():
     with pytest.raises(P.DivergedError):
         tr.read_loss(tr.step(x, tgt))
     assert torch.equal(before, tr.flat.data)
+
+
+def test_device_prefetcher_yields_every_batch():
+    """Each batch arrives intact on the device (checked at its iteration: buffers are reused)."""
+    host = [(torch.full((64, 3), float(i)).pin_memory(), torch.arange(64) + i) for i in range(5)]
+    n = 0
+    for i, (x, y) in enumerate(P.DevicePrefetcher(iter(host), "cuda")):
+        assert x.is_cuda and y.is_cuda
+        assert torch.equal(x.cpu(), host[i][0]) and torch.equal(y.cpu(), host[i][1])
+        torch.cuda._sleep(1000000)  # a slow consumer must not see the next copy land early
+        assert torch.equal(x.cpu(), host[i][0])
+        n += 1
+    assert n == 5
+
+
+def test_capture_rejects_ukan():
+    model = P.build_model("ukan", [3, 2], 3, seed=1, delta_g=0.5, d_pe=8, d_femb=8)
+    tr = P.SplineTrainer(model, "mse", 1e-2)
+    x = torch.zeros((4, 3), device="cuda")
+    with pytest.raises(P.ConfigError):
+        tr.capture(x, torch.zeros((4, 2), device="cuda"))
+
+
+@pytest.mark.parametrize("kind", ["kan"])
+def test_captured_step_matches_eager(kind):
+    """CapturedStep (the step as one CUDA graph, device-side Adam counter) reproduces eager steps."""
+    kw = dict(G=8) if kind == "kan" else dict(delta_g=0.5, d_pe=8, d_femb=8)
+    rng = np.random.default_rng(3)
+    xs = [torch.tensor(rng.uniform(-1, 1, (64, 6)), dtype=torch.float32, device="cuda") for _ in range(4)]
+    ys = [torch.tensor(rng.integers(0, 3, 64), device="cuda") for _ in range(4)]
+    runs = []
+    for use_graph in (False, True):
+        model = P.build_model(kind, [6, 7, 3], 3, seed=5, **kw)
+        tr = P.SplineTrainer(model, "softmax_cross_entropy", 1e-2, "adam", weight_decay=1e-5)
+        losses = [tr.read_loss(tr.step(xs[0], ys[0]))]
+        if use_graph:
+            cap = tr.capture(xs[0], ys[0])
+            losses += [tr.read_loss(cap.replay(xs[s], ys[s])) for s in range(1, 4)]
+            assert cap.sync_step_count() == 4
+        else:
+            losses += [tr.read_loss(tr.step(xs[s], ys[s])) for s in range(1, 4)]
+        runs.append((losses, {n: p.detach().cpu().numpy().copy() for n, p in model.parameters().items()}))
+    (la, pa), (lb, pb) = runs
+    np.testing.assert_allclose(lb, la, rtol=1e-6)
+    for n in pa:
+        np.testing.assert_allclose(pb[n], pa[n], rtol=1e-5, atol=1e-7, err_msg=n)
