@@ -421,6 +421,52 @@ spline_dx_kernel(const float* __restrict__ x, const float* __restrict__ T,
   }
 }
 
+// Same dx with g and scale pre-widened to fp64 (one conversion per element per backward instead
+// of one per (sample, feature, output)): F2F.F64.F32 issues at 1/4 of the DFMA rate, so the
+// per-output conversions of g and scale bound the plain kernel on wide layers.  No base branch.
+__global__ void cvt_f64_kernel(const float* __restrict__ in, double* __restrict__ out, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (double)in[t];
+}
+
+template <int K, bool UKAN>
+__global__ void __launch_bounds__(256)
+spline_dx64_kernel(const float* __restrict__ x, const float* __restrict__ T, const double* __restrict__ s64,
+                   const double* __restrict__ g64, float* __restrict__ dx, int B, int d_in, int d_out, RowMap rm,
+                   Basis<K> bas) {
+  const int lane = threadIdx.x % 32;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (pair >= (int64_t)B * d_in) return;
+  const int i = (int)(pair / B), b = (int)(pair % B);  // feature-major (see spline_dx_kernel)
+  const float xv = x[(size_t)b * d_in + i];
+  int row;
+  double u;
+  bool mask;
+  locate_row<UKAN>(rm, xv, b, i, d_in, row, u, mask);
+  double wp[K];
+  basis_dweights<K>(bas, u, wp);
+  double S[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) S[j] = 0.0;
+  const float* Ti = T + (size_t)row * d_out;
+  const double* gr = g64 + (size_t)b * d_out;
+  const double* sr = s64 + (size_t)i * d_out;
+  for (int o = lane; o < d_out; o += 32) {
+    const double gs = gr[o] * sr[o];  // exact: a product of two fp32 values
+#pragma unroll
+    for (int j = 0; j < K; ++j) S[j] = fma(gs, (double)Ti[(size_t)j * d_out + o], S[j]);
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) t = fma(S[j], wp[j], t);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  if (lane == 0) {
+    const double inv = UKAN ? rm.inv_dg : rm.grid.inv_dg;
+    dx[(size_t)b * d_in + i] = (float)(mask ? t * inv : 0.0);
+  }
+}
+
 __global__ void kan_locate_kernel(const float* __restrict__ x, int32_t* __restrict__ cell,
                                   double* __restrict__ u, int64_t n, KanGrid grid) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -865,10 +911,14 @@ static bool ukan_seg_ok(int64_t B, int64_t d_out, int k) {
   return 2 * B * (k + 1) < ((int64_t)1 << 23) - 64 && seg_supported(B, d_out);
 }
 
+static int64_t ukan_dx64_bytes(int64_t B, int64_t d_in, int64_t d_out) {
+  return (int64_t)sizeof(double) * (B * d_out + d_in * d_out);
+}
+
 extern "C" int64_t ukan_ukan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
                                                      int64_t n_u, int k) {
   if (ukan_seg_ok(B, d_out, k) && getenv("UKAN_UKAN_BWD") == nullptr)
-    return seg_workspace(B, d_in, d_out, n_u * (k + 1));
+    return ((seg_workspace(B, d_in, d_out, n_u * (k + 1)) + 255) / 256) * 256 + ukan_dx64_bytes(B, d_in, d_out);
   return (int64_t)sizeof(double) * n_u * (k + 1) * d_out;
 }
 
@@ -898,9 +948,16 @@ extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
       if (rc) return rc;
       if (dx) {
         const int64_t pairs = B * d_in;
-        spline_dx_kernel<K, true><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, table, scale, nullptr, gy, dx,
-                                                                               (int)B, (int)d_in, (int)d_out, rm,
-                                                                               make_basis<K>(K - 1));
+        double* g64 = reinterpret_cast<double*>(static_cast<unsigned char*>(workspace) +
+                                                ((seg_workspace(B, d_in, d_out, n_u * (k + 1)) + 255) / 256) * 256);
+        double* s64 = g64 + B * d_out;
+        cvt_f64_kernel<<<(unsigned)((B * d_out + 255) / 256), 256, 0, st>>>(gy, g64, B * d_out);
+        UKAN_LAUNCH_CHECK();
+        cvt_f64_kernel<<<(unsigned)((d_in * d_out + 255) / 256), 256, 0, st>>>(scale, s64, d_in * d_out);
+        UKAN_LAUNCH_CHECK();
+        spline_dx64_kernel<K, true><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, table, s64, g64, dx, (int)B,
+                                                                                 (int)d_in, (int)d_out, rm,
+                                                                                 make_basis<K>(K - 1));
         UKAN_LAUNCH_CHECK();
       }
       return UKAN_OK;
