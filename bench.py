@@ -266,6 +266,7 @@ def our_arm(args, rank, world, local_rank):
     e2e_value = world * B * e2e_steps / e2e_s
 
     ukan = ukan_layer_rate(dev) if (world == 1 and not args.no_ukan) else None
+    cfg_rates = kan_layer_rates(dev) if (world == 1 and not args.no_configs) else None
     if rank != 0:
         return
     pk = peaks()
@@ -333,6 +334,7 @@ def our_arm(args, rank, world, local_rank):
                 "h2d_bytes_per_step": B * d0 * 4 + B * 8, "d2h_bytes_per_step": 8 + 4},
         "cpu_baseline": cpu,
         "ukan_layer": ukan,
+        "kan_layers": cfg_rates,
     }
     print(json.dumps(line), flush=True)
 
@@ -364,6 +366,44 @@ def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
             "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "n_u": n_u, "steps": steps, "warmup": warmup}
 
 
+def kan_layer_rates(dev):
+    """Supplementary single-layer KAN measurements at BASELINE configs[0] and configs[2] (SURVEY
+    8d D4): forward + backward of every parameter (x is input data: no dx) through the drop-in
+    API, device-timed (CUDA events), with the FP32/FP64 roof fraction of the layer's algorithmic
+    flops (forward 2KBio on FP32, table gradient 2KBio on FP64)."""
+    import torch
+    import paper_2408_11200_b200 as P
+    out = {}
+    for name, (d, G, B, steps, outl) in {"cfg1": (64, 10, 1024, 50, 0.0), "cfg3": (4096, 64, 65536, 2, 0.01)}.items():
+        layer = P.init_layer("kan", d, d, 3, seed=0, g_min=-1.0, g_max=1.0, G=G, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(3)
+        x = torch.rand((B, d), device=dev, generator=g) * 2 - 1
+        if outl:
+            m = torch.rand((B, d), device=dev, generator=g) < outl
+            x = torch.where(m, x * 3, x)
+        gy = torch.randn((B, d), device=dev, generator=g)
+        params = [layer.coeffs, layer.scale]
+        for _ in range(2):
+            torch.autograd.grad(P.kan_forward(layer, x), params, gy)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            torch.autograd.grad(P.kan_forward(layer, x), params, gy)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        fl = 2.0 * 4 * B * d * d
+        roof_ms = (fl / (FP32_TFLOPS_MEASURED * 1e12) + fl / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3
+        out[name] = {"workload": f"KAN layer {d}->{d} G={G} k=3 B={B}" + (", 1% clamp tail" if outl else "")
+                     + ", fwd + parameter grads", "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms,
+                     "steps": steps, "roof_ms": roof_ms, "roof_frac": roof_ms / ms}
+        del layer, x, gy
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -372,6 +412,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ukan", action="store_true", help="skip the supplementary UKAN layer measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the supplementary cfg1 / cfg3 layer measurements")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
