@@ -278,7 +278,8 @@ def our_arm(args, rank, world, local_rank):
     fwd_ms = kern_ms.get("layer0.kan_forward")
     bwd_ms = kern_ms.get("layer0.kan_backward")
     if bwd_ms and fwd_ms and bwd_ms >= fwd_ms:
-        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 backward: kan_bwd_tc_prep + kan_bwd_tc_sweep (FP64 DMMA)", bwd_ms,
+        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 backward: kan_bwd_tc2_sweep (FP64 DMMA); its x-only record "
+                                                "prep runs earlier on a side stream (ukan_kan_backward_prep)", bwd_ms,
                                                 f_bwd, FP64_TFLOPS_MEASURED, "fp64-fma")
     else:
         dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 forward: kan_pack + kan_fwd_records + kan_fwd_tm (TMEM gather)",
@@ -295,7 +296,8 @@ def our_arm(args, rank, world, local_rank):
     traffic = None
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
-            grp = json.load(f).get("layer0.kan_backward" if "backward" in dom else "layer0.kan_forward")
+            tj = json.load(f)
+            grp = tj.get("layer0.kan_backward_sweep") if "backward" in dom else tj.get("layer0.kan_forward")
         traffic = grp["dram_bytes"] if grp else None
     except (OSError, ValueError, KeyError):
         traffic = None

@@ -82,8 +82,8 @@ int ukan_kan_backward(const float* x, const float* coeffs, const float* scale,
                       int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
                       double g_min, double g_max, void* stream);
 
-/* Same as ukan_kan_backward with an explicit workspace; required (non-zero size) only when
- * the fp64 accumulator of one feature does not fit in shared memory (very large G). */
+/* Same as ukan_kan_backward with an explicit caller workspace (stream-ordered, no allocation
+ * inside; the size query covers every kernel choice). */
 int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t G,
                                          int k);
 int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,
@@ -91,6 +91,22 @@ int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale
                          float* dscale, float* dbase_weight, int64_t B, int64_t d_in,
                          int64_t d_out, int64_t G, int k, double g_min, double g_max,
                          void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Split form of the backward: ukan_kan_backward_prep depends on x only and fills the sorted
+ * per-chunk records of the FP64 tensor-core path into the workspace, so a caller can run it
+ * early on another stream (overlapping the layers above); *prepared (host) is set to 1 when it
+ * launched the prep, 0 when that path does not apply (nothing done).  Pass flags = *prepared to
+ * ukan_kan_backward_ws2 with the same workspace (after the prep's stream work) to reuse them;
+ * flags = 0 is ukan_kan_backward_ws. */
+int ukan_kan_backward_prep(const float* x, const float* base_weight, int64_t B, int64_t d_in,
+                           int64_t d_out, int64_t G, int k, double g_min, double g_max,
+                           void* workspace, int64_t workspace_bytes, int32_t* prepared,
+                           void* stream);
+int ukan_kan_backward_ws2(const float* x, const float* coeffs, const float* scale,
+                          const float* base_weight, const float* gy, float* dx, float* dcoeffs,
+                          float* dscale, float* dbase_weight, int64_t B, int64_t d_in,
+                          int64_t d_out, int64_t G, int k, double g_min, double g_max,
+                          void* workspace, int64_t workspace_bytes, int flags, void* stream);
 
 /* Grid location only (for parity tests / tooling): cell [B, d_in] int32 and u [B, d_in]
  * double exactly as layers.py:296-300 compute them. */

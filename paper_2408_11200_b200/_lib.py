@@ -43,6 +43,9 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_kan_backward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),
     "ukan_kan_backward_ws": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT,
                                     _F64, _F64, _P, _I64, _P]),
+    "ukan_kan_backward_ws2": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64,
+                                     _P, _I64, _INT, _P]),
+    "ukan_kan_backward_prep": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _I64, _P, _P]),
     "ukan_kan_naive_forward": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),
     "ukan_kan_naive_backward": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),
     "ukan_kan_jvp_forward": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),

@@ -576,15 +576,27 @@ static int tc_launch(const float* C, const float* scale, const float* gy, float*
   return UKAN_OK;
 }
 
+// Records only (the first half of kan_bwd_tc_run): lets a caller run the x-only prep early on a
+// side stream, overlapping the layers above, and pass prepared = true to kan_bwd_tc_run.
+int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, int d_in, int G, const KanGrid& grid,
+                    const TcPlan& p, cudaStream_t st) {
+  if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
+  dim3 pg((d_in + 7) / 8, p.nch);
+  kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, reinterpret_cast<unsigned char*>(workspace), B, d_in, p.nch, G, grid);
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
 int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                    void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
-                   const TcPlan& p, cudaStream_t st) {
+                   const TcPlan& p, cudaStream_t st, bool prepared) {
   if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
   unsigned char* recs = reinterpret_cast<unsigned char*>(workspace);
   double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
-  dim3 pg((d_in + 7) / 8, p.nch);
-  kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid);
-  UKAN_LAUNCH_CHECK();
+  if (!prepared) {
+    const int rc = kan_bwd_tc_prep(x, workspace, ws_bytes, B, d_in, G, grid, p, st);
+    if (rc) return rc;
+  }
   if (p.split && p.rb == 8 && p.wpf == 4) return tc2_launch<8, 8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);

@@ -508,7 +508,9 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
 int64_t kan_bwd_tc_workspace(const TcPlan& p);
 int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                    void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
-                   const TcPlan& p, cudaStream_t st);
+                   const TcPlan& p, cudaStream_t st, bool prepared);
+int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, int d_in, int G, const KanGrid& grid,
+                    const TcPlan& p, cudaStream_t st);
 bool kan_bwd_dmma_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base, int sms, RegPlan& p);
 int kan_bwd_dmma_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
                           float* dscale, double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid,
@@ -741,15 +743,19 @@ extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
 }
 
+static const char* kan_bwd_selector() {
+  static const char* sel_env = getenv("UKAN_BWD");
+  return sel_env ? sel_env : "tc";
+}
+
 template <int K>
 static int kan_backward_impl(const float* x, const float* coeffs, const float* scale, const float* bw,
                              const float* gy, float* dx, float* dC, float* dscale, float* dbw, void* workspace,
                              int64_t workspace_bytes, int B, int d_in, int d_out, const RowMap& rm,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool prepared) {
   // UKAN_BWD selects the table-gradient kernel for A/B measurement ("tc" default: banded DMMA,
   // kan_bwd_tc.cu; "sw": register accumulators, kan_bwd_sw.cu; "dmma", "reg": older variants).
-  static const char* sel_env = getenv("UKAN_BWD");
-  const char* sel = sel_env ? sel_env : "tc";
+  const char* sel = kan_bwd_selector();
   bool table_done = false;
   if (sel[0] == 's' && B > 0) {
     const SwPlan sp = kan_bwd_sw_plan(B, d_in, d_out, rm.R, K, bw != nullptr);
@@ -775,7 +781,7 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
     const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, rm.R - K + 1, K - 1, false);
     if (tp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_tc_workspace(tp)) {
       int rc = kan_bwd_tc_run(x, coeffs, scale, gy, dC, dscale, workspace, workspace_bytes, B, d_in, d_out,
-                              rm.R - K + 1, rm.grid, tp, st);
+                              rm.R - K + 1, rm.grid, tp, st, prepared);
       if (rc) return rc;
       if (dx) {
         if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
@@ -834,12 +840,12 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
   return UKAN_OK;
 }
 
-extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,
+extern "C" int ukan_kan_backward_ws2(const float* x, const float* coeffs, const float* scale,
                                    const float* base_weight, const float* gy, float* dx,
                                    float* dcoeffs, float* dscale, float* dbase_weight,
                                    int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
                                    double g_min, double g_max, void* workspace,
-                                   int64_t workspace_bytes, void* stream) {
+                                   int64_t workspace_bytes, int flags, void* stream) {
   int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
   if (rc) return rc;
   if (!coeffs || !scale || !dcoeffs || !dscale || (B > 0 && (!x || !gy))) return UKAN_E_ARG;
@@ -855,8 +861,35 @@ extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const f
       (workspace == nullptr || workspace_bytes < (int64_t)sizeof(double) * d_in * rm.R * d_out))
     return UKAN_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  UKAN_DISPATCH_K(k, return kan_backward_impl<K>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out, rm, st););
+  UKAN_DISPATCH_K(k, return kan_backward_impl<K>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out, rm, st, (flags & 1) != 0););
   return UKAN_OK;
+}
+
+extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,
+                                   const float* base_weight, const float* gy, float* dx,
+                                   float* dcoeffs, float* dscale, float* dbase_weight,
+                                   int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
+                                   double g_min, double g_max, void* workspace,
+                                   int64_t workspace_bytes, void* stream) {
+  return ukan_kan_backward_ws2(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, B, d_in, d_out,
+                               G, k, g_min, g_max, workspace, workspace_bytes, 0, stream);
+}
+
+extern "C" int ukan_kan_backward_prep(const float* x, const float* base_weight, int64_t B, int64_t d_in,
+                                      int64_t d_out, int64_t G, int k, double g_min, double g_max, void* workspace,
+                                      int64_t workspace_bytes, int32_t* prepared, void* stream) {
+  if (prepared == nullptr) return UKAN_E_ARG;
+  *prepared = 0;
+  int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
+  if (rc) return rc;
+  const char* sel = kan_bwd_selector();
+  if (B < 1 || k != 3 || base_weight != nullptr || sel[0] != 't' || x == nullptr) return UKAN_OK;
+  const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, G, k, false);
+  if (!tp.ok || workspace == nullptr || workspace_bytes < kan_bwd_tc_workspace(tp)) return UKAN_OK;
+  rc = kan_bwd_tc_prep(x, workspace, workspace_bytes, (int)B, (int)d_in, (int)G, make_kan_grid(g_min, g_max, G), tp,
+                       (cudaStream_t)stream);
+  if (rc == UKAN_OK) *prepared = 1;
+  return rc;
 }
 
 extern "C" int ukan_kan_backward(const float* x, const float* coeffs, const float* scale,

@@ -166,6 +166,28 @@ class SplineTrainer:
         self.kernel_launches += 4
         return y, (keys, inp, pre, H, table)
 
+    def _prep_first_layer(self, layer, x):
+        """The first layer's backward records depend on x only: build them on a side stream while
+        the layers above run forward and backward (ukan_kan_backward_prep)."""
+        B = x.shape[0]
+        nbytes = self.lib.ukan_kan_backward_workspace_size(B, layer.d_in, layer.d_out, layer.G, layer.k)
+        if nbytes <= 0:
+            return
+        ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        prepared = ctypes.c_int32(0)
+        with torch.cuda.stream(side):
+            check(self.lib.ukan_kan_backward_prep(ptr(x), ptr(layer.base_weight), B, layer.d_in, layer.d_out, layer.G,
+                                                  layer.k, float(layer.g_min), float(layer.g_max), ptr(ws), nbytes,
+                                                  ctypes.byref(prepared), stream_ptr()), "kan_backward_prep")
+        ev = torch.cuda.Event()
+        ev.record(side)
+        self._pre0 = (ws, nbytes, prepared.value == 1, ev)
+        self.kernel_launches += prepared.value
+
     def _bwd(self, i, layer, h, gy, cache, need_dx):
         st = stream_ptr()
         B = h.shape[0]
@@ -173,15 +195,22 @@ class SplineTrainer:
         gv = self.flat.gviews
         dx = torch.empty_like(h) if need_dx else None
         if isinstance(layer, KanLayer):
-            nbytes = self.lib.ukan_kan_backward_workspace_size(B, layer.d_in, layer.d_out, layer.G, layer.k)
-            ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8) if nbytes else None
+            flags = 0
+            if i == 0 and getattr(self, "_pre0", None) is not None:
+                ws, nbytes, prepared, ev = self._pre0
+                torch.cuda.current_stream(self.device).wait_event(ev)
+                flags = 1 if prepared else 0
+                self._pre0 = None
+            else:
+                nbytes = self.lib.ukan_kan_backward_workspace_size(B, layer.d_in, layer.d_out, layer.G, layer.k)
+                ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8) if nbytes else None
             bw = layer.base_weight
             with self._mark(f"layer{i}.kan_backward"):
-              check(self.lib.ukan_kan_backward_ws(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(bw), ptr(gy),
-                                                ptr(dx), ptr(gv[pre_ + "coeffs"]), ptr(gv[pre_ + "scale"]),
-                                                ptr(gv.get(pre_ + "base_weight")) if bw is not None else None,
-                                                B, layer.d_in, layer.d_out, layer.G, layer.k, float(layer.g_min),
-                                                float(layer.g_max), ptr(ws), nbytes, st), "kan_backward")
+              check(self.lib.ukan_kan_backward_ws2(ptr(h), ptr(layer.coeffs), ptr(layer.scale), ptr(bw), ptr(gy),
+                                                 ptr(dx), ptr(gv[pre_ + "coeffs"]), ptr(gv[pre_ + "scale"]),
+                                                 ptr(gv.get(pre_ + "base_weight")) if bw is not None else None,
+                                                 B, layer.d_in, layer.d_out, layer.G, layer.k, float(layer.g_min),
+                                                 float(layer.g_max), ptr(ws), nbytes, flags, st), "kan_backward")
             self.kernel_launches += 2 if need_dx else 1
             return dx
         keys, inp, pre, H, table = cache
@@ -227,11 +256,14 @@ class SplineTrainer:
             self.kernel_launches += 1
         hs = [x]
         caches = []
+        self._pre0 = None
         for li, layer in enumerate(layers):
             self._li = li
             y, cache = self._fwd(layer, hs[-1])
             hs.append(y)
             caches.append(cache)
+            if li == 0 and isinstance(layer, KanLayer) and len(layers) > 1:
+                self._prep_first_layer(layer, x)
         out = hs[-1]
         if self._loss_buf is None or self._loss_buf.numel() < out.numel() + 1:
             self._loss_buf = torch.empty(out.numel() + 1, device=self.device, dtype=torch.float64)

@@ -66,7 +66,9 @@ def test_workspace_queries():
     # segmented sweep: sorted chunk records (256 x 12 B per feature and chunk) + tile starts + fp64
     # dscale partials per 32-row tile (n_u*K rows, plus one partial tile per feature)
     rec, ts, tiles = 4 * 1 * 256 * 12, 256, (10 * 4 + 31) // 32 + 4
-    assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == rec + ts + 8 * tiles * 3
+    # + g and scale widened to fp64 for the dx kernel
+    seg = rec + ts + 8 * tiles * 3
+    assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == (seg + 255) // 256 * 256 + 8 * (8 * 3 + 4 * 3)
 
 
 def test_argument_errors_without_gpu():

@@ -93,6 +93,7 @@ if os.path.exists(rep):
 
     traffic = {"source": f"profiles/ncu_full_{tag}.json (ncu --set full, one launch per kernel, largest of each name)",
                "layer0.kan_backward": _group(["kan_bwd_tc_prep_kernel", "kan_bwd_tc2_sweep_kernel"]),
+               "layer0.kan_backward_sweep": _group(["kan_bwd_tc2_sweep_kernel"]),
                "layer0.kan_forward": _group(["kan_pack_coeffs_kernel", "kan_fwd_records_kernel", "kan_fwd_tm_kernel"])}
     with open(os.path.join(out, "traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
