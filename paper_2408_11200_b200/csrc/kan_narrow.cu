@@ -17,21 +17,20 @@
 
 namespace ukan {
 
-constexpr int kNarrowWarps = 8;
 
-template <int K, int DO>
-__global__ void __launch_bounds__(kNarrowWarps * 32)
+template <int K, int DO, int NW>
+__global__ void __launch_bounds__(NW * 32)
 kan_fwd_narrow_kernel(const float* __restrict__ x, const float* __restrict__ C, const float* __restrict__ scale,
                       const float* __restrict__ bw, float* __restrict__ y, int B, int d_in, int d_out, int R,
                       KanGrid grid, Basis<K> bas, int32_t* __restrict__ err) {
-  __shared__ float part[kNarrowWarps][32][DO + 1];
+  __shared__ float part[NW][32][DO + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 32 + lane;
   const bool live = b < B;
   float acc[DO];
 #pragma unroll
   for (int o = 0; o < DO; ++o) acc[o] = 0.f;
-  for (int i = warp; i < d_in; i += kNarrowWarps) {
+  for (int i = warp; i < d_in; i += NW) {
     const float xv = live ? __ldg(x + (size_t)b * d_in + i) : 0.f;
     int cell;
     double u;
@@ -68,15 +67,15 @@ kan_fwd_narrow_kernel(const float* __restrict__ x, const float* __restrict__ C, 
     if (bb >= B) continue;
     float a = part[0][s][o];
 #pragma unroll
-    for (int w = 1; w < kNarrowWarps; ++w) a += part[w][s][o];
+    for (int w = 1; w < NW; ++w) a += part[w][s][o];
     y[(size_t)bb * d_out + o] = a;
   }
 }
 
 // dx[b,i] = mask * inv_dg * sum_j w'_j * sum_o g[b,o]*scale[i,o]*C[i,cell+j,o]
 //           (+ dsilu(x) * sum_o g[b,o]*bw[i,o])      fp64 products and sums
-template <int K, int DO>
-__global__ void __launch_bounds__(kNarrowWarps * 32)
+template <int K, int DO, int NW>
+__global__ void __launch_bounds__(NW * 32)
 kan_dx_narrow2_kernel(const float* __restrict__ x, const float* __restrict__ C, const float* __restrict__ scale,
                       const float* __restrict__ bw, const float* __restrict__ gy, float* __restrict__ dx, int B,
                       int d_in, int d_out, int R, KanGrid grid, Basis<K> bas) {
@@ -89,7 +88,7 @@ kan_dx_narrow2_kernel(const float* __restrict__ x, const float* __restrict__ C, 
 #pragma unroll
   for (int o = 0; o < DO; ++o) g[o] = (live && o < d_out) ? (double)__ldg(gy + (size_t)b * d_out + o) : 0.0;
   for (int f0 = 0; f0 < d_in; f0 += FT) {
-    for (int fl = warp; fl < FT; fl += kNarrowWarps) {
+    for (int fl = warp; fl < FT; fl += NW) {
       const int i = f0 + fl;
       float res = 0.f;
       if (i < d_in && live) {
@@ -141,9 +140,10 @@ int kan_fwd_narrow(const float* x, const float* C, const float* scale, const flo
   if (B == 0) return UKAN_OK;
   const Basis<K> bas = make_basis<K>(K - 1);
   const dim3 g((B + 31) / 32);
-  if (d_out <= 8) kan_fwd_narrow_kernel<K, 8><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
-  else if (d_out <= 16) kan_fwd_narrow_kernel<K, 16><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
-  else if (d_out <= 32) kan_fwd_narrow_kernel<K, 32><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
+  // 16 warps (more independent feature chains per sample block) where the partial-sum tile fits
+  if (d_out <= 8) kan_fwd_narrow_kernel<K, 8, 16><<<g, 16 * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
+  else if (d_out <= 16) kan_fwd_narrow_kernel<K, 16, 16><<<g, 16 * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
+  else if (d_out <= 32) kan_fwd_narrow_kernel<K, 32, 8><<<g, 8 * 32, 0, st>>>(x, C, scale, bw, y, B, d_in, d_out, R, grid, bas, err);
   else return UKAN_E_ARG;
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
@@ -155,9 +155,9 @@ int kan_dx_narrow2(const float* x, const float* C, const float* scale, const flo
   if (B == 0) return UKAN_OK;
   const Basis<K> bas = make_basis<K>(K - 1);
   const dim3 g((B + 31) / 32);
-  if (d_out <= 8) kan_dx_narrow2_kernel<K, 8><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
-  else if (d_out <= 16) kan_dx_narrow2_kernel<K, 16><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
-  else if (d_out <= 32) kan_dx_narrow2_kernel<K, 32><<<g, kNarrowWarps * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
+  if (d_out <= 8) kan_dx_narrow2_kernel<K, 8, 16><<<g, 16 * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
+  else if (d_out <= 16) kan_dx_narrow2_kernel<K, 16, 16><<<g, 16 * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
+  else if (d_out <= 32) kan_dx_narrow2_kernel<K, 32, 8><<<g, 8 * 32, 0, st>>>(x, C, scale, bw, gy, dx, B, d_in, d_out, R, grid, bas);
   else return UKAN_E_ARG;
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
