@@ -14,7 +14,7 @@ import torch
 from .errors import ConfigError, DomainError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libukan_b200.so")
+LIB_PATH = os.environ.get("UKAN_B200_LIB") or os.path.join(_HERE, "libukan_b200.so")  # override: A/B tooling
 
 UKAN_OK = 0
 UKAN_E_ARG = -1

@@ -380,7 +380,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
       for (int bl = 0; bl < BH; ++bl) {
         const int bb = h * BH + bl;
         const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
-#pragma unroll 2
+#pragma unroll 4
         for (int kc = e0; kc < e1; kc += 4) {
           const int pos = kc + kq;
           const bool vld = pos < e1;
