@@ -251,6 +251,37 @@ cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const f
     drain(c);
   }
 
+  if (mode == 0) {
+    // coalesced epilogue: the thread-per-row accumulators go through shared memory (the pipeline
+    // stages are free once every chunk is drained) so each warp stores contiguous row segments
+    constexpr int TS = BN + 1;  // odd row stride: the row-per-lane writes hit distinct banks
+    float* tile = reinterpret_cast<float*>(smem_raw);
+    __syncthreads();
+    const int r = 32 * q + lane;
+#pragma unroll
+    for (int j = 0; j < HN; ++j) {
+      const int n = n0 + half * HN + j;
+      const float v = (float)acc[j] + ((bias && n < N) ? bias[n] : 0.f);
+      tile[r * TS + half * HN + j] = v;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kTcgM * BN; idx += kTcgThreads) {
+      const int rr = idx / BN, cc = idx % BN;
+      const int mm = m0 + rr, n = n0 + cc;
+      if (mm >= M || n >= N) continue;
+      const float v = tile[rr * TS + cc];
+      if (act) {
+        pre[(size_t)mm * N + n] = v;
+        C[(size_t)mm * N + n] = v / (1.f + __expf(-v));
+      } else {
+        C[(size_t)mm * N + n] = v;
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
+    return;
+  }
   // epilogue: row m, columns n0 + half*HN + j
   const int m = m0 + 32 * q + lane;
   if (m < M) {
