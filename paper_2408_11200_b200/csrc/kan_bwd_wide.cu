@@ -590,6 +590,219 @@ seg_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   }
 }
 
+// seg_dmma (cubic splines): the same tiles on the FP64 tensor cores.  A batch of the tile's samples
+// is counting-sorted by cell (stable), cells are grouped in 4-cell blocks whose windows span 8 rows
+// (stride 4, as kan_bwd_tc.cu), and four samples of a block form the k=4 operand of one
+// mma.sync.m8n8k4.f64 per 8 outputs.  A warp owns 64 outputs and keeps only the current block's
+// 8x64 accumulators: when it moves to the next block the lower 4 rows are complete (retired into an
+// fp64 shared tile) and the upper 4 rows become the next block's lower rows (one shuffle).
+constexpr int kSdW = 4;            // warps per CTA
+constexpr int kSdNT = 8;           // 8-output DMMA tiles per warp
+constexpr int kSdOW = kSdW * 8 * kSdNT;  // outputs per CTA (256)
+constexpr int kSdSB = 256;         // samples per batch
+constexpr int kSdNC = 36;          // cells v = cell - r0 + 4 in [1, 35]; blocks of 4 -> 9
+
+__host__ __device__ constexpr size_t segd_smem_bytes() {
+  return sizeof(double) * ((size_t)kWdRT * kSdOW + (size_t)kSdSB * 4 * 2 + (size_t)kSdSB * 2) +
+         sizeof(int) * (4 * kSdSB + 3 * kSegMaxCh + 2 * kSdNC + 16);
+}
+
+__device__ __forceinline__ void sd_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <bool UKAN>
+__global__ void __launch_bounds__(32 * kSdW)
+seg_dmma_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ T, const float* __restrict__ scale,
+                const float* __restrict__ gy, float* __restrict__ dT, double* __restrict__ part,
+                const int* __restrict__ tile_start, int d_in, int d_out, int nch, int n_og, RowMap rm, Basis<4> bas) {
+  extern __shared__ __align__(16) double sdm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  double* A = sdm;                                   // [32][kSdOW] fp64 tile accumulator
+  double* w_st = A + (size_t)kWdRT * kSdOW;          // [SB][4] staging order
+  double* w_so = w_st + (size_t)kSdSB * 4;           // [SB][4] cell order
+  int* v_st = reinterpret_cast<int*>(w_so + (size_t)kSdSB * 4 + (size_t)kSdSB * 2);
+  int* b_st = v_st + kSdSB;                          // g row offsets, staging order
+  int* pos = b_st + kSdSB;
+  int* b_so = pos + kSdSB;                           // g row offsets, cell order
+  int* c_lo = b_so + kSdSB;                          // [nch]
+  int* c_off = c_lo + kSegMaxCh;                     // [nch + 1]
+  int* cst = c_off + 2 * kSegMaxCh;                  // [kSdNC + 1]
+  const int64_t blk = blockIdx.x;
+  const int og = (int)(blk % n_og);
+  const int tt = (int)(blk / n_og);
+  if (tt >= tile_start[d_in]) return;
+  int lo_f = 0, hi_f = d_in - 1;
+  while (lo_f < hi_f) {
+    const int mid = (lo_f + hi_f + 1) >> 1;
+    if (tile_start[mid] <= tt) lo_f = mid;
+    else hi_f = mid - 1;
+  }
+  const int i = lo_f;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  const int r0 = (tt - tile_start[i]) * kWdRT;
+  const int lo_key = max(0, r0 - 3) << 8, hi_key = (r0 + kWdRT) << 8;
+  const int ob = og * kSdOW + warp * (8 * kSdNT);  // this warp's first output
+  for (int c = warp; c < nch; c += kSdW) {
+    const int4* e4 = reinterpret_cast<const int4*>(recs + ((size_t)i * nch + c) * (kWdBC * 12)) + lane * 2;
+    const int4 ka = __ldg(e4), kb = __ldg(e4 + 1);
+    int nlo = (ka.x < lo_key) + (ka.y < lo_key) + (ka.z < lo_key) + (ka.w < lo_key) + (kb.x < lo_key) +
+              (kb.y < lo_key) + (kb.z < lo_key) + (kb.w < lo_key);
+    int nhi = (ka.x < hi_key) + (ka.y < hi_key) + (ka.z < hi_key) + (ka.w < hi_key) + (kb.x < hi_key) +
+              (kb.y < hi_key) + (kb.z < hi_key) + (kb.w < hi_key);
+    nlo = __reduce_add_sync(0xffffffffu, nlo);
+    nhi = __reduce_add_sync(0xffffffffu, nhi);
+    if (lane == 0) {
+      c_lo[c] = nlo;
+      c_off[c + 1] = nhi - nlo;
+    }
+  }
+  for (int t = threadIdx.x; t < kWdRT * kSdOW; t += blockDim.x) A[t] = 0.0;
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      int v = c < nch ? c_off[c + 1] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += t;
+      }
+      if (c < nch) c_off[c + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) c_off[0] = 0;
+  }
+  __syncthreads();
+  const int N = c_off[nch];
+  for (int s0 = 0; s0 < N; s0 += kSdSB) {
+    const int nb = min(kSdSB, N - s0);
+    // a. stage in chunk order: cell v, basis weights, g row offset
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+      const int gq = s0 + q;
+      int lo = 0, hi = nch - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (c_off[mid] <= gq) lo = mid;
+        else hi = mid - 1;
+      }
+      const int c = lo;
+      const int p = c_lo[c] + (gq - c_off[c]);
+      const unsigned char* rec = recs + ((size_t)i * nch + c) * (kWdBC * 12);
+      const int key = __ldg(reinterpret_cast<const int*>(rec) + p);
+      double w[4];
+      basis_weights<4>(bas, __ldg(reinterpret_cast<const double*>(rec + kWdBC * 4) + p), w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w_st[q * 4 + j] = w[j];
+      v_st[q] = (key >> 8) - r0 + 4;
+      b_st[q] = (c * kWdBC + (key & 255)) * d_out;
+    }
+    __syncthreads();
+    // b. stable counting sort by cell (warps split the cells)
+    for (int c = warp; c < kSdNC; c += kSdW) {
+      int n = 0;
+      for (int q0 = 0; q0 < nb; q0 += 32) {
+        const int q = q0 + lane;
+        n += __popc(__ballot_sync(0xffffffffu, q < nb && v_st[q] == c));
+      }
+      if (lane == 0) cst[c + 1] = n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cst[0] = 0;
+      for (int c = 0; c < kSdNC; ++c) cst[c + 1] += cst[c];
+    }
+    __syncthreads();
+    for (int c = warp; c < kSdNC; c += kSdW) {
+      int base = cst[c];
+      for (int q0 = 0; q0 < nb; q0 += 32) {
+        const int q = q0 + lane;
+        const bool m = q < nb && v_st[q] == c;
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        if (m) pos[q] = base + __popc(bal & ((1u << lane) - 1u));
+        base += __popc(bal);
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+      const int ps = pos[q];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w_so[ps * 4 + j] = w_st[q * 4 + j];
+      b_so[ps] = b_st[q];
+    }
+    __syncthreads();
+    // c. DMMA sweep block by block (cells 4b .. 4b+3 -> rows v = 4b .. 4b+7)
+    double acc[kSdNT][2];
+#pragma unroll
+    for (int t = 0; t < kSdNT; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int bk = 0; bk < kSdNC / 4; ++bk) {
+      const int e0 = cst[4 * bk], e1 = cst[4 * bk + 4];
+#pragma unroll 2
+      for (int kc = e0; kc < e1; kc += 4) {
+        const int si = kc + kq;
+        const bool vld = si < e1;
+        const int sc = vld ? si : e0;
+        int vs = 0;
+        // the sample's cell: cst is monotone; recover v from the block-local cell boundaries
+#pragma unroll
+        for (int cc = 1; cc < 4; ++cc) vs += (sc >= cst[4 * bk + cc]) ? 1 : 0;
+        const int jj = grp - vs;  // row offset inside the sample's window
+        const double a = (vld && jj >= 0 && jj < 4) ? w_so[sc * 4 + (jj & 3)] : 0.0;
+        const float* gr = gy + (size_t)(unsigned)b_so[sc] + ob + grp;
+        double bf[kSdNT];
+#pragma unroll
+        for (int t = 0; t < kSdNT; ++t) {
+          const int o = ob + t * 8 + grp;
+          bf[t] = (vld && o < d_out) ? (double)__ldg(gr + t * 8) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kSdNT; ++t) sd_dmma(acc[t][0], acc[t][1], a, bf[t]);
+      }
+      // retire rows v = 4bk .. 4bk+3 (tile rows 4bk-4 .. 4bk-1), slide the upper half down
+      const int r = 4 * bk - 4 + grp;
+      if (grp < 4 && r >= 0) {
+#pragma unroll
+        for (int t = 0; t < kSdNT; ++t) {
+          double* a2 = A + (size_t)r * kSdOW + warp * (8 * kSdNT) + t * 8 + 2 * kq;
+          a2[0] += acc[t][0];
+          a2[1] += acc[t][1];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kSdNT; ++t) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const double up = __shfl_xor_sync(0xffffffffu, acc[t][v], 16);
+          acc[t][v] = grp < 4 ? up : 0.0;
+        }
+      }
+    }
+    // rows v = 36 .. 39 would be tile rows 32 .. 35: outside the tile, dropped
+    __syncthreads();
+  }
+  // d. epilogue: dT = scale * A, dscale partial = sum_r T * A  (this warp's 64 outputs, 2 per lane)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int oc = warp * (8 * kSdNT) + h * 32 + lane;
+    const int o = og * kSdOW + oc;
+    if (o >= d_out) continue;
+    const double scl = (double)__ldg(scale + (size_t)i * d_out + o);
+    double prod = 0.0;
+    for (int rr = 0; rr < kWdRT && r0 + rr < nrows; ++rr) {
+      const double a = A[(size_t)rr * kSdOW + oc];
+      const size_t ci = (size_t)(row0 + r0 + rr) * d_out + o;
+      dT[ci] = (float)(scl * a);
+      prod = fma((double)__ldg(T + ci), a, prod);
+    }
+    part[(size_t)tt * d_out + o] = prod;
+  }
+}
+
 // dscale[f,o] = sum over the feature's tiles (fixed order)
 __global__ void seg_reduce_kernel(const double* __restrict__ part, const int* __restrict__ tile_start,
                                   float* __restrict__ dscale, int d_in, int d_out) {
@@ -627,6 +840,22 @@ int seg_table_grad(const float* x, const float* T, const float* scale, const flo
   UKAN_LAUNCH_CHECK();
   seg_tiles_kernel<UKAN><<<1, 32, 0, st>>>(rm, d_in, tile_start);
   UKAN_LAUNCH_CHECK();
+  static const bool cuda_cores = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == '1';  // A/B only
+  if constexpr (K == 4) {
+    if (!cuda_cores) {
+      const int n_og = (d_out + kSdOW - 1) / kSdOW;
+      const size_t smem = segd_smem_bytes();
+      UKAN_CUDA_TRY(cudaFuncSetAttribute(seg_dmma_kernel<UKAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      seg_dmma_kernel<UKAN><<<(unsigned)(tiles * n_og), 32 * kSdW, smem, st>>>(
+          recs, T, scale, gy, dT, part, tile_start, d_in, d_out, nch, n_og, rm, make_basis<4>(3));
+      UKAN_LAUNCH_CHECK();
+      const int64_t n = (int64_t)d_in * d_out;
+      seg_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, tile_start, dscale, d_in, d_out);
+      UKAN_LAUNCH_CHECK();
+      return UKAN_OK;
+    }
+  }
   const int n_os = (d_out + 31) / 32;
   const int W = std::min(8, n_os);
   const int n_og = (n_os + W - 1) / W;
