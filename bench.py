@@ -267,6 +267,7 @@ def our_arm(args, rank, world, local_rank):
 
     ukan = ukan_layer_rate(dev) if (world == 1 and not args.no_ukan) else None
     cfg_rates = kan_layer_rates(dev) if (world == 1 and not args.no_configs) else None
+    pinn = pinn_rate(dev) if (world == 1 and not args.no_configs) else None
     if rank != 0:
         return
     pk = peaks()
@@ -337,6 +338,7 @@ def our_arm(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "ukan_layer": ukan,
         "kan_layers": cfg_rates,
+        "pinn": pinn,
     }
     print(json.dumps(line), flush=True)
 
@@ -403,6 +405,34 @@ def kan_layer_rates(dev):
                      "steps": steps, "roof_ms": roof_ms, "roof_frac": roof_ms / ms}
         del layer, x, gy
         torch.cuda.empty_cache()
+    return out
+
+
+def pinn_rate(dev, n_colloc=128, steps=50, warmup=5):
+    """Supplementary F2 measurement: one PINN step (pinn_loss through the forward-tangent kernels of
+    a [1, 5, 1] KAN and a [1, 5, 1] UKAN, tasks.py:153-166, plus the reverse pass through the
+    tangent graph), device-timed; tiny and launch-bound by nature."""
+    import numpy as np
+    import torch
+    import paper_2408_11200_b200 as P
+    out = {}
+    for kind, kw in (("kan", dict(g_min=-5.0, g_max=5.0, G=10)), ("ukan", dict(delta_g=0.5, d_pe=8, d_femb=8))):
+        model = P.build_model(kind, [1, 5, 1], 3, seed=0, device=dev, **kw)
+        prob = P.PinnProblem(1.0, -5.0, 5.0, n_colloc)
+        colloc = torch.tensor(prob.sample_collocation(np.random.default_rng(1)), dtype=torch.float32, device=dev)
+        params = list(model.parameters().values())
+        for _ in range(warmup):
+            torch.autograd.grad(P.pinn_loss(model.forward, prob, colloc), params)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            torch.autograd.grad(P.pinn_loss(model.forward, prob, colloc), params)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        out[kind] = {"workload": f"pinn_loss [1,5,1] {kind}, {n_colloc} collocation points, loss + parameter grads",
+                     "ms_per_step": ms, "collocation_points_per_s": n_colloc / (ms * 1e-3)}
     return out
 
 
