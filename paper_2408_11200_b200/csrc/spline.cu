@@ -743,6 +743,29 @@ extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int
   return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
 }
 
+// A side stream per (host thread, device) to overlap two independent small kernels of one call:
+// fork / join through events recorded on the caller's stream, which is also how a stream under
+// CUDA-graph capture pulls the side stream into the graph.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  thread_local SideStream ss[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  SideStream& r = ss[dev];
+  if (r.s == nullptr) {
+    if (cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming) != cudaSuccess) {
+      r.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &r;
+}
+
 static const char* kan_bwd_selector() {
   static const char* sel_env = getenv("UKAN_BWD");
   return sel_env ? sel_env : "tc";
@@ -780,9 +803,19 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
   if (sel[0] == 't' && K == 4 && bw == nullptr && B > 0) {  // FP64 tensor-core path (kan_bwd_tc.cu)
     const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, rm.R - K + 1, K - 1, false);
     if (tp.ok && workspace != nullptr && workspace_bytes >= kan_bwd_tc_workspace(tp)) {
+      SideStream* ss = (dx && d_out <= 32) ? side_stream() : nullptr;
+      if (ss) {  // narrow layer: dx (independent of the table gradient) on the side stream
+        UKAN_CUDA_TRY(cudaEventRecord(ss->fork, st));
+        UKAN_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+        int rc = kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, ss->s);
+        if (rc) return rc;
+        UKAN_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+      }
       int rc = kan_bwd_tc_run(x, coeffs, scale, gy, dC, dscale, workspace, workspace_bytes, B, d_in, d_out,
                               rm.R - K + 1, rm.grid, tp, st, prepared);
+      if (ss) UKAN_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
       if (rc) return rc;
+      if (ss) return UKAN_OK;
       if (dx) {
         if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
         const Basis<K> bas = make_basis<K>(K - 1);
