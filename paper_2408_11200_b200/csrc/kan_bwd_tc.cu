@@ -509,6 +509,12 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
     p.nt = 8;
     p.fpb = 4;
   }
+  static const int rb16_wpf = getenv("UKAN_TC2_RB16_WPF") ? atoi(getenv("UKAN_TC2_RB16_WPF")) : 4;
+  if (p.split && p.rb == 16 && rb16_wpf == 4) {  // 16 warps: 4 features x 4 block parts, NT = 4
+    p.wpf = 4;
+    p.nt = 4;
+    p.fpb = 4;
+  }
   const int opb = 8 * p.nt;
   const int fpb = p.split ? p.fpb : 8;
   p.nch = (int)((B + kTcBC - 1) / kTcBC);
@@ -601,6 +607,7 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
   if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16 && p.wpf == 4) return tc2_launch<16, 4, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16) return tc2_launch<16, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
