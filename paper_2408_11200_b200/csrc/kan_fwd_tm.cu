@@ -197,7 +197,10 @@ constexpr int kTmSDepth = 5;  // shared-memory ring: TMA loads run up to 3 stage
 // measured at ~6 B/clk for this shape) and computes the current stage: per sample one
 // tcgen05.ld of the K*4-word window + K*4 FFMA.  The only barrier per stage is a 4-warp
 // named barrier per lane quarter (TMEM double buffer).
-template <int K, int SW>
+// DEPTH: shared-memory ring depth (5, or 3 when the slabs of finer grids do not fit five times);
+// DB: two TMEM slab buffers (the next feature's fill overlaps this feature's gathers) when two
+// slabs of RP x 4 columns fit the 512 TMEM columns, else one buffer refilled after a barrier.
+template <int K, int SW, int DEPTH, bool DB>
 __global__ void __launch_bounds__(kTmThreads, 1)
 kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, const float* __restrict__ rw,
                   float* __restrict__ y, int B, int Bp, int d_in, int d_out, int RP, int fpc) {
@@ -209,7 +212,7 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
   static_assert(2 * kTmWarpsQ * SW == kTmST && SW % 4 == 0, "tile shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t full_s[kTmSDepth], empty_s[kTmSDepth];
+  __shared__ __align__(8) uint64_t full_s[DEPTH], empty_s[DEPTH];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, ws = warp >> 2;
@@ -230,18 +233,18 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (producer) {
-    for (int d = 0; d < kTmSDepth; ++d) {
+    for (int d = 0; d < DEPTH; ++d) {
       mb_init(&full_s[d], 1);
       mb_init(&empty_s[d], NWARP);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   const float* cp_ot = Cp + (size_t)ot * d_in * RP * kTmOT;
-  auto buf_ptr = [&](int g) { return smem_raw + (size_t)(g % kTmSDepth) * buf_bytes; };
+  auto buf_ptr = [&](int g) { return smem_raw + (size_t)(g % DEPTH) * buf_bytes; };
   auto issue_loads = [&](int g) {  // slab + records of stage g -> shared buffer g % 5
     unsigned char* d = buf_ptr(g);
     const int i = i_lo + g;
-    uint64_t* mb = &full_s[g % kTmSDepth];
+    uint64_t* mb = &full_s[g % DEPTH];
     mb_expect_tx(mb, buf_bytes);
     bulk_g2s(d, cp_ot + (size_t)i * RP * kTmOT, slab_bytes, mb);
     bulk_g2s(d + slab_bytes, rw + ((size_t)i * Bp + b0) * KP, recw_bytes, mb);
@@ -251,7 +254,7 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
   auto pump = [&](int upto) {  // loads for stages < upto whose buffer has been released
     for (; next_load < min(upto, nstage); ++next_load) {
       const int g = next_load;
-      if (g >= kTmSDepth) mb_wait(&empty_s[g % kTmSDepth], (uint32_t)(((g - kTmSDepth) / kTmSDepth) & 1));
+      if (g >= DEPTH) mb_wait(&empty_s[g % DEPTH], (uint32_t)(((g - DEPTH) / DEPTH) & 1));
       issue_loads(g);
     }
   };
@@ -271,10 +274,10 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
   // this warp's rows of a slab -> TMEM buffer (g & 1), lanes of its quarter
   auto fill = [&](int g) {
     const float4* src = reinterpret_cast<const float4*>(buf_ptr(g)) + slot;
-    const uint32_t cbase = tl + (uint32_t)((g & 1) * RP * OV);
+    const uint32_t cbase = tl + (uint32_t)((DB ? (g & 1) : 0) * RP * OV);
     for (int r = ws; r < RP; r += kTmWarpsQ) tm_st4(cbase + (uint32_t)(r * OV), src[(size_t)r * (kTmOT / 4)]);
   };
-  if (producer) pump(kTmSDepth - 1);
+  if (producer) pump(DEPTH - 1);
   __syncwarp();
   if (nstage > 0) {
     mb_wait(&full_s[0], 0);
@@ -287,17 +290,17 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
 
   const int sb = (cg * kTmWarpsQ + ws) * SW;
   for (int g = 0; g < nstage; ++g) {
-    const int ds = g % kTmSDepth;
-    if (producer) pump(g + kTmSDepth - 1);
+    const int ds = g % DEPTH;
+    if (producer) pump(g + DEPTH - 1);
     __syncwarp();
-    if (g + 1 < nstage) {  // stage g+1 -> the other TMEM buffer (freed by the last quarter barrier)
-      mb_wait(&full_s[(g + 1) % kTmSDepth], (uint32_t)(((g + 1) / kTmSDepth) & 1));
+    if (DB && g + 1 < nstage) {  // stage g+1 -> the other TMEM buffer (freed by the last quarter barrier)
+      mb_wait(&full_s[(g + 1) % DEPTH], (uint32_t)(((g + 1) / DEPTH) & 1));
       fill(g + 1);
     }
     const unsigned char* bp = buf_ptr(g);  // stage g landed: waited before its fill
     const float* wr = reinterpret_cast<const float*>(bp + slab_bytes) + (size_t)sb * KP;
     const uint8_t* cr = bp + slab_bytes + recw_bytes + sb;
-    const uint32_t tcol = tl + (uint32_t)((g & 1) * RP * OV);
+    const uint32_t tcol = tl + (uint32_t)((DB ? (g & 1) : 0) * RP * OV);
     // two samples per TMEM wait; the cells of four samples come in one 32-bit load
 #pragma unroll
     for (int s = 0; s < SW; s += 4) {
@@ -333,6 +336,14 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     tm_fence_before();
     asm volatile("bar.sync %0, %1;\n" ::"r"(qbar), "r"(kTmWarpsQ * 32) : "memory");
     tm_fence_after();
+    if (!DB && g + 1 < nstage) {  // single TMEM buffer: refill after every warp of the quarter is done
+      mb_wait(&full_s[(g + 1) % DEPTH], (uint32_t)(((g + 1) / DEPTH) & 1));
+      fill(g + 1);
+      tm_wait_st();
+      tm_fence_before();
+      asm volatile("bar.sync %0, %1;\n" ::"r"(qbar), "r"(kTmWarpsQ * 32) : "memory");
+      tm_fence_after();
+    }
   }
 
   // epilogue: y (or this split's partial) for SW samples x OV outputs
@@ -377,6 +388,7 @@ struct TmPlan {
   int RP = 0, fpc = 0, S = 1, n_ot = 0, Bp = 0;
   size_t smem = 0;
   int64_t pack_bytes = 0, rec_bytes = 0, part_bytes = 0;
+  int depth = kTmSDepth, db = 1;
 };
 
 TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base) {
@@ -387,10 +399,16 @@ TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   while (nw < K * 4) nw *= 2;
   if (nw > 32) return p;
   const int rp = (int)(G - 1) + nw / 4;  // rows reachable by a window load
-  if (2 * rp * 4 > 512) return p;  // two stages of one feature must fit TMEM
+  if (rp * 4 > 512) return p;     // one stage of one feature must fit TMEM
   const int KP = (K + 3) / 4 * 4;
   p.RP = rp;
-  p.smem = (size_t)kTmSDepth * ((size_t)rp * kTmOT * 4 + (size_t)kTmST * KP * 4 + kTmST);
+  const size_t per = (size_t)rp * kTmOT * 4 + (size_t)kTmST * KP * 4 + kTmST;
+  p.depth = (size_t)kTmSDepth * per <= 220 * 1024 ? kTmSDepth : 3;
+  // two TMEM stages (the next fill overlaps the gathers) need two slabs in TMEM and the deep ring
+  // (with a 3-deep ring the early fill waits on its TMA load: G=48 measured 10.1 ms double- vs
+  // 8.9 ms single-buffered at B=16384, 1024->1024, slower than G=64 single-buffered)
+  p.db = (2 * rp * 4 <= 512 && p.depth == kTmSDepth) ? 1 : 0;
+  p.smem = (size_t)p.depth * per;
   if (p.smem > 220 * 1024) return p;
   p.n_ot = (int)((d_out + kTmOT - 1) / kTmOT);
   p.Bp = (int)((B + kTmST - 1) / kTmST * kTmST);
@@ -430,7 +448,8 @@ static int launch_tm(const float* x, const float* C, const float* scale, float* 
   kan_fwd_records_kernel<K><<<dim3((B + 31) / 32, (d_in + 31) / 32), 256, 0, st>>>(x, recc, recw, B, p.Bp, d_in, grid,
                                                                                    make_basis<K>(K - 1), err);
   UKAN_LAUNCH_CHECK();
-  auto kern = kan_fwd_tm_kernel<K, SW>;
+  auto kern = p.depth == kTmSDepth ? (p.db ? kan_fwd_tm_kernel<K, SW, kTmSDepth, true> : kan_fwd_tm_kernel<K, SW, kTmSDepth, false>)
+                                    : (p.db ? kan_fwd_tm_kernel<K, SW, 3, true> : kan_fwd_tm_kernel<K, SW, 3, false>);
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 gridd(p.Bp / kTmST, p.n_ot, p.S);
   float* out = p.S > 1 ? part : y;

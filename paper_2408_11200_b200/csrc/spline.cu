@@ -532,6 +532,7 @@ struct TmPlan {
   int RP = 0, fpc = 0, S = 1, n_ot = 0, Bp = 0;
   size_t smem = 0;
   int64_t pack_bytes = 0, rec_bytes = 0, part_bytes = 0;
+  int depth = 5, db = 1;
 };
 TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
 int64_t kan_fwd_tm_workspace(const TmPlan& p);
