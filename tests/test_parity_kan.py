@@ -194,3 +194,10 @@ def test_fine_grid_clustered_cells():
     b = run_layer(layer, x, gup)
     for key in a:
         np.testing.assert_array_equal(a[key], b[key])
+
+
+@pytest.mark.parametrize("G", [37, 48, 64])
+def test_tmem_forward_fine_grid_variants(G):
+    """TMEM-gather forward around its plan boundaries: G=37 (5-deep ring, two TMEM slabs), G=48
+    (3-deep ring, one slab) and G=64 (one slab of 67 x 4 columns); d_out >= 128 takes that path."""
+    check_against_oracle(*random_case(300, 5, 130, 3, G, seed=60 + G, outliers=0.05), need_dx=False)
