@@ -803,6 +803,185 @@ seg_dmma_kernel(const unsigned char* __restrict__ recs, const float* __restrict_
   }
 }
 
+// seg_f*: one sorted pass per feature.  seg_fsort_kernel merges a feature's chunk records into one
+// stable order by (row, chunk, sample) with a row histogram in shared memory; seg_fsweep_kernel
+// then walks the feature's rows once in 4-cell blocks on the FP64 tensor cores with an 8-row
+// register window (as seg_dmma), retiring every row exactly once straight into dT, and reduces
+// dscale in registers — no per-tile staging, no fp64 tile in shared memory, no dscale partials.
+constexpr int kFsMaxRows = 48 * 1024;  // per-feature rows the shared histogram holds
+
+template <bool UKAN>
+__global__ void __launch_bounds__(256)
+seg_fsort_kernel(const unsigned char* __restrict__ recs, int nch, int d_in, RowMap rm, int* __restrict__ row_start,
+                 int* __restrict__ sorted_b, double* __restrict__ sorted_u, int B) {
+  extern __shared__ int cnt[];  // [nrows + 1] histogram -> starts -> cursors
+  __shared__ int ks[kWdBC];
+  const int i = blockIdx.x;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  int* rs = row_start + row0 + i;  // [nrows + 1]
+  int* sb = sorted_b + (size_t)i * B;
+  double* su = sorted_u + (size_t)i * B;
+  for (int r = threadIdx.x; r <= nrows; r += blockDim.x) cnt[r] = 0;
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int* ent = reinterpret_cast<const int*>(recs + ((size_t)i * nch + c) * (kWdBC * 12));
+    for (int p = threadIdx.x; p < kWdBC; p += blockDim.x) {
+      const int row = __ldg(ent + p) >> 8;
+      if (row < nrows) atomicAdd(&cnt[row], 1);  // padding / NaN keys carry a row beyond the segment
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan (one warp, 32 rows per step)
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int r0 = 0; r0 <= nrows; r0 += 32) {
+      const int r = r0 + lane;
+      const int v = r < nrows ? cnt[r] : 0;
+      int inc = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
+      }
+      if (r <= nrows) {
+        cnt[r] = carry + inc - v;
+        rs[r] = carry + inc - v;
+      }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {  // chunks in sample order; inside a chunk keys are sorted by (row, sample)
+    const unsigned char* rec = recs + ((size_t)i * nch + c) * (kWdBC * 12);
+    for (int p = threadIdx.x; p < kWdBC; p += blockDim.x) ks[p] = __ldg(reinterpret_cast<const int*>(rec) + p);
+    __syncthreads();
+    for (int p = threadIdx.x; p < kWdBC; p += blockDim.x) {
+      const int key = ks[p], row = key >> 8;
+      if (row >= nrows) continue;
+      int lo = 0, hi = p;  // first position of this row in the chunk
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((ks[mid] >> 8) < row) lo = mid + 1;
+        else hi = mid;
+      }
+      const int pos = cnt[row] + (p - lo);
+      sb[pos] = c * kWdBC + (key & 255);
+      su[pos] = __ldg(reinterpret_cast<const double*>(rec + kWdBC * 4) + p);
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < kWdBC; p += blockDim.x) {  // run ends advance the row cursors
+      const int row = ks[p] >> 8;
+      if (row >= nrows) continue;
+      if (p + 1 == kWdBC || (ks[p + 1] >> 8) != row) {
+        int lo = 0, hi = p;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((ks[mid] >> 8) < row) lo = mid + 1;
+          else hi = mid;
+        }
+        cnt[row] += p - lo + 1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kFsW = 4;   // warps per CTA
+constexpr int kFsNT = 8;  // 8-output DMMA tiles per warp (64 outputs)
+
+template <bool UKAN>
+__global__ void __launch_bounds__(32 * kFsW)
+seg_fsweep_kernel(const int* __restrict__ row_start, const int* __restrict__ sorted_b,
+                  const double* __restrict__ sorted_u, const float* __restrict__ T, const float* __restrict__ scale,
+                  const float* __restrict__ gy, float* __restrict__ dT, float* __restrict__ dscale, int d_in,
+                  int d_out, int B, RowMap rm, Basis<4> bas) {
+  __shared__ double Msh[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  __syncthreads();
+  const int i = blockIdx.y;
+  const int ob = (blockIdx.x * kFsW + warp) * (8 * kFsNT);
+  if (ob >= d_out) return;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  const int* rs = row_start + row0 + i;
+  const int* sb = sorted_b + (size_t)i * B;
+  const double* su = sorted_u + (size_t)i * B;
+  double acc[kFsNT][2], prod[kFsNT][2];
+  float scl[kFsNT][2];
+#pragma unroll
+  for (int t = 0; t < kFsNT; ++t)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      acc[t][v] = prod[t][v] = 0.0;
+      const int o = ob + t * 8 + 2 * kq + v;
+      scl[t][v] = o < d_out ? __ldg(scale + (size_t)i * d_out + o) : 0.f;
+    }
+  const int nblk = (nrows + 3) / 4;
+  int c0 = __ldg(rs + 0);
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int c1 = __ldg(rs + min(4 * bb + 1, nrows)), c2 = __ldg(rs + min(4 * bb + 2, nrows)),
+              c3 = __ldg(rs + min(4 * bb + 3, nrows)), c4 = __ldg(rs + min(4 * bb + 4, nrows));
+    for (int kc = c0; kc < c4; kc += 4) {
+      const int si = kc + kq;
+      const bool vld = si < c4;
+      const int sc = vld ? si : kc;
+      const int vs = (sc >= c1) + (sc >= c2) + (sc >= c3);
+      const int jj = grp - vs;
+      const double u = __ldg(su + sc);
+      const int j3 = jj & 3;
+      const double wj = fma(fma(fma(Msh[12 + j3], u, Msh[8 + j3]), u, Msh[4 + j3]), u, Msh[j3]);
+      const double a = (vld && jj >= 0 && jj < 4) ? wj : 0.0;
+      const float* gr = gy + (size_t)__ldg(sb + sc) * d_out + ob + grp;
+      double bf[kFsNT];
+#pragma unroll
+      for (int t = 0; t < kFsNT; ++t) bf[t] = (vld && ob + t * 8 + grp < d_out) ? (double)__ldg(gr + t * 8) : 0.0;
+#pragma unroll
+      for (int t = 0; t < kFsNT; ++t) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[t][0]), "+d"(acc[t][1])
+                     : "d"(a), "d"(bf[t]));
+      }
+    }
+    // rows 4bb .. 4bb+3 are complete: dT, the dscale products, then slide the upper half down
+    const int row = 4 * bb + grp;
+    if (grp < 4 && row < nrows) {
+#pragma unroll
+      for (int t = 0; t < kFsNT; ++t)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int o = ob + t * 8 + 2 * kq + v;
+          if (o < d_out) {
+            const size_t ci = (size_t)(row0 + row) * d_out + o;
+            dT[ci] = (float)((double)scl[t][v] * acc[t][v]);
+            prod[t][v] = fma((double)__ldg(T + ci), acc[t][v], prod[t][v]);
+          }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kFsNT; ++t)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const double up = __shfl_xor_sync(0xffffffffu, acc[t][v], 16);
+        acc[t][v] = grp < 4 ? up : 0.0;
+      }
+    c0 = c4;
+  }
+  // dscale: sum the four row residues (grp 0..3) in a fixed order
+#pragma unroll
+  for (int t = 0; t < kFsNT; ++t)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      double d = prod[t][v];
+      d += __shfl_xor_sync(0xffffffffu, d, 4);
+      d += __shfl_xor_sync(0xffffffffu, d, 8);
+      const int o = ob + t * 8 + 2 * kq + v;
+      if (lane < 4 && o < d_out) dscale[(size_t)i * d_out + o] = (float)d;
+    }
+}
+
 // dscale[f,o] = sum over the feature's tiles (fixed order)
 __global__ void seg_reduce_kernel(const double* __restrict__ part, const int* __restrict__ tile_start,
                                   float* __restrict__ dscale, int d_in, int d_out) {
@@ -822,7 +1001,8 @@ int64_t seg_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t total_rows
   const int64_t rec = ((d_in * nch * kWdBC * 12 + 255) / 256) * 256;
   const int64_t ts = ((4 * (d_in + 1) + 255) / 256) * 256;
   const int64_t tiles = (total_rows + kWdRT - 1) / kWdRT + d_in;
-  return rec + ts + (int64_t)sizeof(double) * tiles * d_out;
+  const int64_t sorted = ((int64_t)12 * d_in * B + 255) / 256 * 256 + ((4 * (total_rows + d_in + 1)) + 255) / 256 * 256;
+  return rec + ts + ((int64_t)sizeof(double) * tiles * d_out + 255) / 256 * 256 + sorted;
 }
 
 template <int K, bool UKAN>
@@ -841,7 +1021,26 @@ int seg_table_grad(const float* x, const float* T, const float* scale, const flo
   seg_tiles_kernel<UKAN><<<1, 32, 0, st>>>(rm, d_in, tile_start);
   UKAN_LAUNCH_CHECK();
   static const bool cuda_cores = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == '1';  // A/B only
+  static const bool tiles_only = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == 't';  // A/B only
+  const int64_t max_rows = std::min<int64_t>(total_rows, 2 * (int64_t)B * K);
   if constexpr (K == 4) {
+    if (!cuda_cores && !tiles_only && max_rows + 1 <= kFsMaxRows) {
+      unsigned char* base = recs + rec + ((4 * ((int64_t)d_in + 1) + 255) / 256) * 256 +
+                            ((int64_t)sizeof(double) * tiles * d_out + 255) / 256 * 256;
+      double* sorted_u = reinterpret_cast<double*>(base);
+      int* sorted_b = reinterpret_cast<int*>(base + (int64_t)8 * d_in * B);
+      int* row_start = reinterpret_cast<int*>(base + ((int64_t)12 * d_in * B + 255) / 256 * 256);
+      const size_t smem = sizeof(int) * (size_t)(max_rows + 1);
+      UKAN_CUDA_TRY(cudaFuncSetAttribute(seg_fsort_kernel<UKAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      seg_fsort_kernel<UKAN><<<d_in, 256, smem, st>>>(recs, nch, d_in, rm, row_start, sorted_b, sorted_u, B);
+      UKAN_LAUNCH_CHECK();
+      const int n_og = (d_out + 8 * kFsNT * kFsW - 1) / (8 * kFsNT * kFsW);
+      seg_fsweep_kernel<UKAN><<<dim3(n_og, d_in), 32 * kFsW, 0, st>>>(row_start, sorted_b, sorted_u, T, scale, gy, dT,
+                                                                      dscale, d_in, d_out, B, rm, make_basis<4>(3));
+      UKAN_LAUNCH_CHECK();
+      return UKAN_OK;
+    }
     if (!cuda_cores) {
       const int n_og = (d_out + kSdOW - 1) / kSdOW;
       const size_t smem = segd_smem_bytes();

@@ -66,8 +66,10 @@ def test_workspace_queries():
     # segmented sweep: sorted chunk records (256 x 12 B per feature and chunk) + tile starts + fp64
     # dscale partials per 32-row tile (n_u*K rows, plus one partial tile per feature)
     rec, ts, tiles = 4 * 1 * 256 * 12, 256, (10 * 4 + 31) // 32 + 4
+    # + per-feature sorted order (sample 4 B + u 8 B per (feature, sample)) and row starts
+    al = lambda n: (n + 255) // 256 * 256  # noqa: E731
+    seg = rec + ts + al(8 * tiles * 3) + al(12 * 4 * 8) + al(4 * (10 * 4 + 4 + 1))
     # + g and scale widened to fp64 for the dx kernel
-    seg = rec + ts + 8 * tiles * 3
     assert lib.ukan_ukan_backward_workspace_size(8, 4, 3, 10, 3) == (seg + 255) // 256 * 256 + 8 * (8 * 3 + 4 * 3)
 
 
