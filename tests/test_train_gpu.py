@@ -95,3 +95,28 @@ def test_captured_step_matches_eager(kind):
     np.testing.assert_allclose(lb, la, rtol=1e-6)
     for n in pa:
         np.testing.assert_allclose(pb[n], pa[n], rtol=1e-5, atol=1e-7, err_msg=n)
+
+
+def test_captured_step_learning_rate_change():
+    """CapturedStep.set_lr changes the device-side rate the graph reads (the reference changes the
+    rate per epoch, train.py:153)."""
+    rng = np.random.default_rng(4)
+    xs = [torch.tensor(rng.uniform(-1, 1, (32, 5)), dtype=torch.float32, device="cuda") for _ in range(3)]
+    ys = [torch.tensor(rng.integers(0, 2, 32), device="cuda") for _ in range(3)]
+    runs = []
+    for use_graph in (False, True):
+        model = P.build_model("kan", [5, 2], 3, seed=9, G=6)
+        tr = P.SplineTrainer(model, "softmax_cross_entropy", 1e-2, "adam")
+        tr.read_loss(tr.step(xs[0], ys[0]))
+        if use_graph:
+            cap = tr.capture(xs[0], ys[0])
+            cap.set_lr(5e-3)
+            tr.read_loss(cap.replay(xs[1], ys[1]))
+            cap.set_lr(1e-3)
+            tr.read_loss(cap.replay(xs[2], ys[2]))
+        else:
+            tr.read_loss(tr.step(xs[1], ys[1], lr=5e-3))
+            tr.read_loss(tr.step(xs[2], ys[2], lr=1e-3))
+        runs.append({n: p.detach().cpu().numpy().copy() for n, p in model.parameters().items()})
+    for n in runs[0]:
+        np.testing.assert_allclose(runs[1][n], runs[0][n], rtol=1e-5, atol=1e-7, err_msg=n)
