@@ -891,7 +891,7 @@ constexpr int kFsW = 4;   // warps per CTA
 constexpr int kFsNT = 8;  // 8-output DMMA tiles per warp (64 outputs)
 
 template <bool UKAN>
-__global__ void __launch_bounds__(32 * kFsW)
+__global__ void __launch_bounds__(32 * kFsW, 8)  // occupancy over registers: latency-bound gathers (ncu A/B: 1 -> 8 blocks/SM = 6.8 -> 4.2 ms despite spills)
 seg_fsweep_kernel(const int* __restrict__ row_start, const int* __restrict__ sorted_b,
                   const double* __restrict__ sorted_u, const float* __restrict__ T, const float* __restrict__ scale,
                   const float* __restrict__ gy, float* __restrict__ dT, float* __restrict__ dscale, int d_in,
