@@ -149,7 +149,7 @@ __device__ __forceinline__ void tc_cp4(void* smem, const void* gmem, bool ok) {
 }
 
 template <int RB, int NT>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, (RB <= 8 && NT <= 2) ? 2 : 1)  // narrow outputs: latency-bound, 2 blocks/SM (layer-1 backward 0.207 -> 0.167 ms)
 kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C,
                         const float* __restrict__ scale, const float* __restrict__ gy,
                         float* __restrict__ dC, float* __restrict__ dscale, double* __restrict__ part,
