@@ -331,6 +331,41 @@ __global__ void __launch_bounds__(256) cg_colsum_part_kernel(const float* __rest
     part[(size_t)blockIdx.y * N + c] = s;
   }
 }
+// float4 variant (N % 4 == 0, 16-byte aligned rows): a lane sums 4 adjacent columns, two rows in
+// flight per iteration (fixed order: even rows then odd rows of the lane's stride, then the warps)
+__global__ void __launch_bounds__(256) cg_colsum_part4_kernel(const float* __restrict__ X, double* __restrict__ part,
+                                                              int K, int N, int rows_per_slice) {
+  __shared__ double red[8][132];
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 128 + lane * 4;
+  const int k0 = blockIdx.y * rows_per_slice, k1 = min(K, k0 + rows_per_slice);
+  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+  if (c < N) {
+    int k = k0 + ty;
+    for (; k + 8 < k1; k += 16) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(X + (size_t)k * N + c));
+      const float4 v = __ldg(reinterpret_cast<const float4*>(X + (size_t)(k + 8) * N + c));
+      a[0] += (double)u.x; a[1] += (double)u.y; a[2] += (double)u.z; a[3] += (double)u.w;
+      b[0] += (double)v.x; b[1] += (double)v.y; b[2] += (double)v.z; b[3] += (double)v.w;
+    }
+    if (k < k1) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(X + (size_t)k * N + c));
+      a[0] += (double)u.x; a[1] += (double)u.y; a[2] += (double)u.z; a[3] += (double)u.w;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[ty][lane * 4 + j] = a[j] + b[j];
+  __syncthreads();
+  if (ty == 0 && c < N) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (int q = 0; q < 8; ++q) s += red[q][lane * 4 + j];
+      part[(size_t)blockIdx.y * N + c + j] = s;
+    }
+  }
+}
+
 __global__ void cg_colsum_final_kernel(const double* __restrict__ part, float* __restrict__ out, int N, int S) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
@@ -382,12 +417,16 @@ bool cg_tc_applicable(const void* a, const void* b, int64_t M, int64_t N, int64_
 }
 
 int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st) {
-  const int64_t cblk = (N + 31) / 32;
+  const bool v4 = (N % 4 == 0) && ((uintptr_t)X % 16 == 0);
+  const int64_t cblk = v4 ? (N + 127) / 128 : (N + 31) / 32;
   const int S = (int)std::max<int64_t>(1, std::min<int64_t>((4 * kan_num_sms() + cblk - 1) / cblk, (K + 255) / 256));
   const int rps = (int)((K + S - 1) / S);
   void* part = nullptr;
   UKAN_CUDA_TRY(scratch_alloc(&part, sizeof(double) * S * N, st));
-  cg_colsum_part_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
+  if (v4)
+    cg_colsum_part4_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
+  else
+    cg_colsum_part_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
   UKAN_LAUNCH_CHECK();
   cg_colsum_final_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(static_cast<double*>(part), out, (int)N, S);
   UKAN_LAUNCH_CHECK();
