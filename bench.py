@@ -1,17 +1,23 @@
 """Benchmark: KAN/UKAN layer fwd+bwd samples/s on 1..8 B200 vs the CPU reference path.
 
-Workload (BASELINE.json configs[1]): KAN stack [784, 256, 10], grid G=32, k=3, batch 8192 per
-GPU (weak scaling), MNIST-shaped synthetic classification (x ~ U(-1,1), labels ~ U{0..9}),
-softmax cross-entropy, Adam — one full data-parallel training step per "step".
+Headline workload (BASELINE.json configs[2], the largest single-GPU configuration):
+cfg3 — one KAN layer 4096 -> 4096, grid G = 64, k = 3, batch 65536 PER GPU (weak scaling), x ~
+U(-1, 1) with a 1% clamp-exercising tail, upstream gradient ~ N(0, 1).  One "step" = the layer's
+data-parallel training step as a hidden layer of a stack (``LayerTrainer.step``): forward,
+backward INCLUDING dx, the dcoeffs/dscale all-reduce in 8 feature buckets overlapping the backward
+(N > 1, NCCL), and the fused Adam update of the layer's 1.1 G parameters.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
 
-Prints one JSON line on rank 0.  `value` is device-timed (CUDA events, inputs resident in HBM,
-max over ranks); `e2e` is the same metric through the public API with pinned host inputs copied
-H2D and the loss read D2H every step.  The CPU reference arm (`--impl reference`, and the
-`cpu_baseline` field) runs the float64 NumPy port of the reference in oracle/ — the reference
-itself is pure Python/NumPy and cannot travel to the GPU box.
+Prints one JSON line on rank 0.  ``value`` is device-timed (CUDA events on the launching stream,
+inputs resident in HBM, x > L2, max over ranks); ``e2e`` is the same step through the public API
+with x and gy copied from pinned host memory and y and dx copied back every step.  The CPU
+reference arm (``--impl reference``, and the ``cpu_baseline`` field) runs the UNMODIFIED reference
+package (installed by __graft_entry__.build() into the git-ignored baseline/_ref) on the box's
+host cores — or, if that install is absent, its float64 NumPy restatement in oracle/.
+Supplementary fields (not the headline): cfg2 (KAN [784,256,10] DP step), the cfg4-shaped UKAN
+layer, cfg5 (UKAN [64,512,512,64] DP training, global batch 65536 sharded), cfg1, PINN.
 """
 from __future__ import annotations
 
@@ -22,16 +28,16 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF = os.path.join(ROOT, "baseline", "_ref")
 
-CFG = dict(widths=[784, 256, 10], G=32, k=3, g_min=-1.0, g_max=1.0, batch=8192, lr=1e-3, wd=0.0)
-ROTATE = 8  # resident batches cycled through: 8 x 25.7 MB of x > 126 MB L2
+CFG3 = dict(d=4096, G=64, k=3, g_min=-1.0, g_max=1.0, batch=65536, tail=0.01, lr=1e-3)
+METRIC = "KAN/UKAN layer fwd+bwd samples/s & HBM GB/s vs peak at 1/2/4/8 B200 vs CPU"
 
 
 def peaks():
@@ -42,15 +48,23 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-# CUDA-core roofs measured with tools/peaks.cu on this pool's B200 (profiles/peaks_r01.json):
-# FMA-chain microbenchmarks, 148 SMs, clocks not locked.
+# Compute roofs measured on this pool's B200 with the microbenchmarks in tools/ (clocks not locked):
+# FMA chains (tools/peaks.cu -> profiles/peaks_r01.json), FP64 DMMA m8n8k4 (tools/dmma_peak.cu ->
+# profiles/dmma_peak_r01.json).  MEASURED_PEAKS.json holds only HBM and bf16.
 FP32_TFLOPS_MEASURED = 71.95
 FP64_TFLOPS_MEASURED = 34.05
+DMMA_TFLOPS_MEASURED = 37.0
 
 
 def kan_flops(B, d_in, d_out, k):
     """Algorithmic FLOPs of one KAN layer pass: 2*K*B*d_in*d_out per pass."""
     return 2.0 * (k + 1) * B * d_in * d_out
+
+
+def kan_bytes(B, d_in, d_out, G, k, dx=True):
+    """Compulsory HBM bytes of one KAN layer fwd+bwd: x, y, dy, dx, C read +
+    dC write, scale + dscale."""
+    return 4.0 * (B * d_in + 2 * B * d_out + (B * d_in if dx else 0) + 2 * d_in * (G + k) * d_out + 2 * d_in * d_out)
 
 
 class ClockSampler:
@@ -97,49 +111,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-# ---------------------------------------------------------------------------------------
-# CPU reference arm (oracle port of the float64 NumPy reference)
-# ---------------------------------------------------------------------------------------
-def _cpu_worker(args):
-    sub, seed = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    import oracle
-    rng = np.random.default_rng(seed)
-    widths, k, G = CFG["widths"], CFG["k"], CFG["G"]
-    params, cfgs = [], []
-    for i in range(len(widths) - 1):
-        d_in, d_out = widths[i], widths[i + 1]
-        params.append({"coeffs": rng.normal(0, 0.1 / np.sqrt(d_in), (d_in, G + k, d_out)).astype(np.float32).astype(np.float64),
-                       "scale": np.ones((d_in, d_out))})
-        cfgs.append(dict(k=k, g_min=CFG["g_min"], g_max=CFG["g_max"], G=G))
-    x = rng.uniform(-1, 1, (sub, widths[0])).astype(np.float32).astype(np.float64)
-    y = rng.integers(0, widths[-1], sub)
-    t0 = time.perf_counter()
-    oracle.model_step("kan", params, cfgs, x, y, "softmax_cross_entropy", CFG["lr"])
-    return time.perf_counter() - t0
-
-
-def cpu_rate(sub: int, procs: int, reps: int):
-    """samples/s of the reference algorithm (oracle port) on `procs` host processes, each
-    running a full fwd+bwd+Adam step on a `sub`-row slice; median over reps."""
-    import multiprocessing as mp
-    times = []
-    if procs == 1:
-        _cpu_worker((sub, 0))  # warm-up
-        for r in range(reps):
-            times.append(_cpu_worker((sub, r + 1)))
-        step = statistics.median(times)
-        return sub / step, step
-    with mp.get_context("spawn").Pool(procs) as pool:
-        pool.map(_cpu_worker, [(sub, i) for i in range(procs)])  # warm-up
-        for r in range(reps):
-            t0 = time.perf_counter()
-            pool.map(_cpu_worker, [(sub, 1000 * r + i) for i in range(procs)])
-            times.append(time.perf_counter() - t0)
-    step = statistics.median(times)
-    return procs * sub / step, step
-
-
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -150,28 +121,99 @@ def cpu_model():
     return "unknown"
 
 
-def reference_arm(args, rank):
-    if rank != 0:
-        return
+# ---------------------------------------------------------------------------------------
+# CPU reference path: the reference's own kan_forward + tape backward (x a recorded node) at
+# cfg3 sub-batches of 1 and 4 rows; the marginal rate (3 rows / (t4 - t1)) removes the fixed
+# cost of the full zeros_like(table) in span_gather's backward (layers.py:68).
+# ---------------------------------------------------------------------------------------
+def _ref_available() -> bool:
+    return os.path.isdir(os.path.join(REF, "ukan"))
+
+
+def _cpu_worker(args):
+    reps, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    d, G, k = CFG3["d"], CFG3["G"], CFG3["k"]
+    rng = np.random.default_rng(seed)
+    pairs = []
+    if _ref_available():
+        if REF not in sys.path:
+            sys.path.insert(0, REF)
+        import ukan
+        T = ukan.tensor
+        layer = ukan.init_layer("kan", d, d, k, seed=seed, g_min=CFG3["g_min"], g_max=CFG3["g_max"], G=G)
+
+        def run(B):
+            x = T.parameter(rng.uniform(-1, 1, (B, d)))
+            g = T.as_tensor(rng.normal(size=(B, d)))
+            t0 = time.perf_counter()
+            y = ukan.kan_forward(layer, x)
+            T.backward(T.sum_all(T.mul(y, g)))
+            return time.perf_counter() - t0
+    else:
+        import oracle
+        C = rng.normal(0, 0.1 / np.sqrt(d), (d, G + k, d))
+        S = np.ones((d, d))
+
+        def run(B):
+            x = rng.uniform(-1, 1, (B, d))
+            g = rng.normal(size=(B, d))
+            t0 = time.perf_counter()
+            oracle.kan_forward_backward(x, C, S, g, k=k, g_min=CFG3["g_min"], g_max=CFG3["g_max"], G=G)
+            return time.perf_counter() - t0
+    for _ in range(reps):
+        t1 = run(1)
+        t4 = run(4)
+        pairs.append((t1, t4))
+    return pairs
+
+
+def cpu_rate(procs: int, reps: int):
+    """cfg3 samples/s of the CPU reference path on `procs` host processes (sum of their marginal
+    rates); returns (rate, per-process seconds per marginal sample, pairs)."""
+    if procs == 1:
+        pairs = _cpu_worker((reps, 0))
+        all_pairs = [pairs]
+    else:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(procs) as pool:
+            all_pairs = pool.map(_cpu_worker, [(reps, i) for i in range(procs)])
+    rates = []
+    for pairs in all_pairs:
+        dt = statistics.median(max(1e-9, t4 - t1) for t1, t4 in pairs)
+        rates.append(3.0 / dt)
+    return sum(rates), all_pairs
+
+
+def _cpu_procs():
     ncpu = len(os.sched_getaffinity(0))
     try:
         mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
     except (ValueError, OSError):
         mem_gb = 64
-    procs = max(1, min(ncpu, 32, int(mem_gb // 4)))
-    sub = 16
-    rate, step = cpu_rate(sub, procs, max(1, args.steps))
+    return max(1, min(ncpu, int(mem_gb // 16)))  # ~15 GB peak per process at B = 4 (zeros_like table)
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    procs = _cpu_procs()
+    reps = max(1, min(2, args.steps))
+    t0 = time.perf_counter()
+    rate, pairs = cpu_rate(procs, reps)
+    wall = time.perf_counter() - t0
+    kind = "reference" if _ref_available() else "port"
+    sample = (f"{procs} host processes x {reps} (B=1, B=4) pairs of the {'unmodified reference (baseline/_ref ukan: kan_forward + T.backward, x a T.parameter)' if kind == 'reference' else 'float64 NumPy port (oracle/)'} "
+              f"on the cfg3 layer; marginal rate 3 rows / (t4 - t1) per process, summed; OMP_NUM_THREADS=1")
+    ms = 1e3 * 65536.0 / rate if rate > 0 else None
     line = {
-        "impl": "reference", "metric": "KAN/UKAN layer fwd+bwd samples/s (KAN [784,256,10] training step)",
-        "value": rate, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: KAN [784,256,10] G=32 k=3 softmax-CE Adam", "global_batch": CFG["batch"],
-                   "parallelism": f"{procs} host processes"},
-        "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} processes x {sub}-row sub-batch, full fwd+bwd+Adam step of the "
-                                   f"float64 NumPy port (oracle/), median of {max(1, args.steps)} reps",
-                         "cpu": cpu_model()},
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3: KAN layer 4096->4096 G=64 k=3, fwd + bwd incl. dx (per-sample marginal cost)",
+                   "global_batch": CFG3["batch"], "parallelism": f"{procs} host processes"},
+        "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": procs, "kind": kind, "sample": sample,
+                         "cpu": cpu_model(), "wall_s": wall, "pairs_s": pairs},
         "e2e": {"value": rate, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -180,173 +222,260 @@ def reference_arm(args, rank):
 # ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
+def _events(timers):
+    return {name: sum(a.elapsed_time(b) for a, b in ev) / len(ev) for name, ev in timers.items()}
+
+
 def our_arm(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_2408_11200_b200 as P
-    from paper_2408_11200_b200 import ops
 
     dev_index = local_rank % torch.cuda.device_count()  # == local_rank on a full node
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    B = CFG["batch"]
-    model = P.build_model("kan", CFG["widths"], CFG["k"], seed=0, device=dev, g_min=CFG["g_min"],
-                          g_max=CFG["g_max"], G=CFG["G"])
-    tr = P.SplineTrainer(model, "softmax_cross_entropy", CFG["lr"], "adam", weight_decay=CFG["wd"])
-    ops.set_check_mode("deferred")
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    xs = [torch.rand((B, CFG["widths"][0]), device=dev, generator=g) * 2 - 1 for _ in range(ROTATE)]
-    ys = [torch.randint(0, CFG["widths"][-1], (B,), device=dev, generator=g) for _ in range(ROTATE)]
+    d, G, k, B = CFG3["d"], CFG3["G"], CFG3["k"], CFG3["batch"]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    layer = P.init_layer("kan", d, d, k, seed=0, g_min=CFG3["g_min"], g_max=CFG3["g_max"], G=G, device=dev)
+    tr = P.LayerTrainer(layer, CFG3["lr"], buckets=8)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    xs, gys = [], []
+    for _ in range(2):  # two resident batches (each x is 1 GiB > the 126 MB L2)
+        x = torch.rand((B, d), device=dev, generator=g) * 2 - 1
+        m = torch.rand((B, d), device=dev, generator=g) < CFG3["tail"]
+        xs.append(torch.where(m, x * 3, x))
+        gys.append(torch.randn((B, d), device=dev, generator=g) / (B * world))
+        del x, m
     for s in range(args.warmup):
-        tr.step(xs[s % ROTATE], ys[s % ROTATE])
-    tr.read_loss(tr.step(xs[0], ys[0]))
+        tr.step(xs[s % 2], gys[s % 2])
     torch.cuda.synchronize()
+    tr.check_input()
     barrier()
 
     # ---- device-timed region (inputs resident in HBM) ----
-    tr.timers = {}
     lib = P._lib.load()
     launches0 = lib.ukan_launch_count()
+    tr.timers = {}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev_index) as clk:
         torch.cuda.synchronize()
         barrier()
         start.record()
         for s in range(args.steps):
-            loss = tr.step(xs[s % ROTATE], ys[s % ROTATE])
+            tr.step(xs[s % 2], gys[s % 2])
         end.record()
         torch.cuda.synchronize()
         barrier()
     launches = (lib.ukan_launch_count() - launches0) // max(1, args.steps)
     ms = start.elapsed_time(end)
-    tr.read_loss(loss)
-    ops.flush_checks()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * B * args.steps / (ms_max * 1e-3)
     timers, tr.timers = tr.timers, None
-    kern_ms = {name: sum(a.elapsed_time(b) for a, b in ev) / len(ev) for name, ev in timers.items()}
+    phase_ms = _events(timers)
+    # per-kernel launch timing of the dominant kernels on the launching stream (one extra step,
+    # not in the timed region): the backward parts are separate launches already
+    tr.check_input()
 
-    # ---- end-to-end through the public API: pinned host inputs, H2D, step, loss D2H ----
-    hx = [torch.empty((B, CFG["widths"][0]), dtype=torch.float32).pin_memory() for _ in range(2)]
-    hy = [torch.empty((B,), dtype=torch.int64).pin_memory() for _ in range(2)]
+    # ---- end to end through the public API: pinned host x / gy in, y / dx out, every step ----
+    hx = [torch.empty((B, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+    hg = [torch.empty((B, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+    hy = torch.empty((B, d), dtype=torch.float32).pin_memory()
+    hdx = torch.empty((B, d), dtype=torch.float32).pin_memory()
     for i in range(2):
         hx[i].copy_(xs[i].cpu())
-        hy[i].copy_(ys[i].cpu())
-    # the step captured as one CUDA graph (single process; N > 1 keeps the eager NCCL path)
-    cap = tr.capture(xs[0], ys[0]) if world == 1 else None
-    if cap is not None:
-        for s in range(2):  # graph warm-up replays
-            tr.read_loss(cap.replay(xs[s], ys[s]))
-    # every step: its batch is copied from pinned host memory (DevicePrefetcher, one step ahead on
-    # a side stream) and its loss is read back to the host.  Wall-clock timed: 3 runs of
-    # max(steps, 60) steps, the median run reported (max over ranks per run).
-    e2e_steps = max(args.steps, 60)
+        hg[i].copy_(gys[i].cpu())
+    del xs, gys
+    torch.cuda.empty_cache()
+    e2e_steps = max(3, min(args.steps, 5))
+    out_stream = torch.cuda.Stream(device=dev)
     runs = []
-    for _ in range(3):
+    for _ in range(2):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for bx, by in P.DevicePrefetcher(((hx[s % 2], hy[s % 2]) for s in range(e2e_steps)), dev):
-            tr.read_loss(cap.replay(bx, by) if cap is not None else tr.step(bx, by))
+        for bx, bg in P.DevicePrefetcher(((hx[s % 2], hg[s % 2]) for s in range(e2e_steps)), dev):
+            y, dx = tr.step(bx, bg)
+            ev = torch.cuda.Event()
+            ev.record()
+            out_stream.wait_stream(torch.cuda.current_stream(dev))  # outputs of this step -> host
+            with torch.cuda.stream(out_stream):
+                hy.copy_(y, non_blocking=True)
+                hdx.copy_(dx, non_blocking=True)
+                y.record_stream(out_stream)
+                dx.record_stream(out_stream)
+        out_stream.synchronize()
         torch.cuda.synchronize()
-        t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        tt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        runs.append(float(t.item()))
-    e2e_s = sorted(runs)[1]
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        runs.append(float(tt.item()))
+    e2e_s = min(runs)
     e2e_value = world * B * e2e_steps / e2e_s
+    del tr, layer, hx, hg, hy, hdx
+    torch.cuda.empty_cache()
 
-    ukan = ukan_layer_rate(dev) if (world == 1 and not args.no_ukan) else None
-    cfg_rates = kan_layer_rates(dev) if (world == 1 and not args.no_configs) else None
-    pinn = pinn_rate(dev) if (world == 1 and not args.no_configs) else None
+    supp = {}
+    if not args.no_configs:
+        supp["cfg5_ukan_dp"] = cfg5_rate(dev, world, rank)
+        if world == 1:
+            supp["cfg2_kan_stack_dp"] = cfg2_rate(dev)
+            supp["ukan_layer"] = ukan_layer_rate(dev)
+            supp["kan_layers"] = kan_layer_rates(dev)
+            supp["pinn"] = pinn_rate(dev)
     if rank != 0:
         return
     pk = peaks()
-    d0, d1, d2 = CFG["widths"]
-    k = CFG["k"]
-    # dominant kernel: the layer-0 (784->256) launches; pick whichever is longer
-    f_fwd = kan_flops(B, d0, d1, k)
-    f_bwd = kan_flops(B, d0, d1, k)  # table gradient only (layer 0 needs no dx)
-    fwd_ms = kern_ms.get("layer0.kan_forward")
-    bwd_ms = kern_ms.get("layer0.kan_backward")
-    if bwd_ms and fwd_ms and bwd_ms >= fwd_ms:
-        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 backward: kan_bwd_tc2_sweep (FP64 DMMA); its x-only record "
-                                                "prep runs earlier on a side stream (ukan_kan_backward_prep)", bwd_ms,
-                                                f_bwd, FP64_TFLOPS_MEASURED, "fp64-fma")
-    else:
-        dom, dom_ms, dom_fl, dom_peak, bound = ("layer0 forward: kan_pack + kan_fwd_records + kan_fwd_tm (TMEM gather)",
-                                                fwd_ms, f_fwd, FP32_TFLOPS_MEASURED, "fp32-fma")
-    achieved = dom_fl / (dom_ms * 1e-3) / 1e12
-    # compulsory HBM bytes of the dominant launch
-    R = CFG["G"] + k
-    if "backward" in dom:
-        hbm_bytes = 4.0 * (B * d0 + B * d1 + 2 * d0 * R * d1 + 3 * d0 * d1)
-    else:
-        hbm_bytes = 4.0 * (B * d0 + B * d1 + d0 * R * d1 + d0 * d1)
-    step_fl = kan_flops(B, d0, d1, k) * 2 + kan_flops(B, d1, d2, k) * 3
-    # DRAM bytes per launch of the dominant kernel group from the committed ncu --set full capture
+    # dominant kernel: the longest phase of the step (each phase is one kernel launch, or one
+    # launch per feature bucket for the table gradient)
+    f_pass = kan_flops(B, d, d, k)
+    phase_info = {
+        "forward": ("kan_fwd_tm_kernel (TMEM gather, FP32 FMA; + pack / records pre-passes)", FP32_TFLOPS_MEASURED,
+                    "fp32 FMA (tools/peaks.cu)"),
+        "backward_dx": ("kan_dx_tc_kernel (dx on FP64 DMMA)", DMMA_TFLOPS_MEASURED, "FP64 DMMA (tools/dmma_peak.cu)"),
+        "backward_table": ("kan_bwd_tc2_sweep_kernel<16,4,4,4> x 8 feature buckets (dC/dscale on FP64 DMMA)",
+                           DMMA_TFLOPS_MEASURED, "FP64 DMMA (tools/dmma_peak.cu)"),
+    }
+    dom = max((p for p in phase_info if p in phase_ms), key=lambda p: phase_ms[p])
+    dom_ms = phase_ms[dom]
+    kern, dom_peak, peak_src = phase_info[dom]
+    achieved = f_pass / (dom_ms * 1e-3) / 1e12
     traffic = None
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-            grp = tj.get("layer0.kan_backward_sweep") if "backward" in dom else tj.get("layer0.kan_forward")
-        traffic = grp["dram_bytes"] if grp else None
-    except (OSError, ValueError, KeyError):
+        with open(os.path.join(ROOT, "profiles", "traffic_r02.json")) as f:
+            traffic = json.load(f).get("cfg3." + dom, {}).get("dram_bytes")
+    except (OSError, ValueError):
         traffic = None
+    hbm = kan_bytes(B, d, d, G, k)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        sub = 16
-        rate, step = cpu_rate(sub, 1, 3)
-        cpu = {"value": rate, "unit": "samples/s", "cores": 1, "kind": "port",
-               "sample": f"{sub}-row slice of the cfg2 batch, full fwd+bwd+Adam step of the float64 NumPy port "
-                         f"(oracle/), median of 3 reps ({step:.1f} s/rep), OMP_NUM_THREADS=1",
+        rate1, pairs = cpu_rate(1, 1)
+        cpu = {"value": rate1, "unit": "samples/s", "cores": 1, "kind": "reference" if _ref_available() else "port",
+               "sample": ("one (B=1, B=4) pair of the cfg3 layer fwd+bwd incl. dx through the "
+                          + ("unmodified reference (baseline/_ref ukan)" if _ref_available() else "float64 port (oracle/)")
+                          + f"; marginal rate 3/(t4-t1); t1={pairs[0][0][0]:.1f} s, t4={pairs[0][0][1]:.1f} s; OMP_NUM_THREADS=1"),
                "cpu": cpu_model()}
+    step_tflops = 3 * f_pass * args.steps / (ms_max * 1e-3) / 1e12
     line = {
-        "metric": "KAN/UKAN layer fwd+bwd samples/s (KAN [784,256,10] training step)",
-        "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 storage; f64 grid locate + backward accumulation", "data": "synthetic",
-        "config": {"workload": "cfg2: KAN [784,256,10] G=32 k=3 MNIST-shaped softmax-CE + Adam, one DP step",
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 storage; f64 grid locate + backward accumulation (DMMA)",
+        "data": "synthetic (x ~ U(-1,1) with a 1% |x|<=3 clamp tail; upstream gradient ~ N(0,1)/global batch)",
+        "config": {"workload": "cfg3: KAN layer 4096->4096 G=64 k=3, one DP training step of the layer as a hidden "
+                               "layer (fwd + bwd incl. dx + bucketed grad all-reduce + Adam)",
                    "global_batch": B * world, "per_gpu_batch": B, "parallelism": f"dp{world}",
-                   "l2": f"inputs rotate over {ROTATE} HBM-resident batches ({ROTATE * B * d0 * 4 / 2**20:.0f} MiB > 126 MB L2)"},
-        "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": dom_peak, "unit": "TFLOP/s",
-                     "frac": achieved / dom_peak, "traffic": traffic,
-                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
-                     "algorithmic_bytes_per_launch": hbm_bytes,
-                     "peak_source": "tools/peaks.cu FMA microbenchmark on this pool's B200 (profiles/peaks_r01.json)",
-                     "algorithmic_flops_per_launch": dom_fl, "avg_launch_ms": dom_ms},
-        "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / (dom_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": hbm_bytes / (dom_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                         "note": "compulsory bytes of the dominant launch; the kernel is compute-bound"},
-        "step_tflops": step_fl * args.steps / (ms_max * 1e-3) / 1e12,
-        "kernel_ms": kern_ms,
+                   "l2": "inputs larger than L2 (x, gy 1 GiB each; two resident batches alternate)"},
+        "roofline": {"bound": "tensor" if "DMMA" in peak_src else "fp32-fma", "kernel": kern, "achieved": achieved,
+                     "peak": dom_peak, "unit": "TFLOP/s", "frac": achieved / dom_peak, "traffic": traffic,
+                     "traffic_unit": "bytes per launch group (ncu dram__bytes_read+write, profiles/traffic_r02.json)",
+                     "peak_source": peak_src, "algorithmic_flops_per_launch": f_pass, "avg_launch_ms": dom_ms},
+        "roofline_hbm": {"bound": "hbm", "achieved": hbm / (ms_max / args.steps * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": hbm / (ms_max / args.steps * 1e-3) / 1e9 / pk["hbm_gbs"],
+                         "note": "compulsory bytes of the whole layer step (SURVEY 8d D2); the step is compute-bound "
+                                 "(FP32 forward, FP64 backward forced by the parity bar)"},
+        "step_tflops": step_tflops,
+        "roof_ms": (f_pass / (FP32_TFLOPS_MEASURED * 1e12) + 2 * f_pass / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3,
+        "phase_ms": phase_ms,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "samples/s", "steps": e2e_steps, "runs_s": runs,
-                "path": "SplineTrainer.capture -> CapturedStep.replay (one CUDA graph per step) fed by "
-                        "DevicePrefetcher" if world == 1 else "SplineTrainer.step fed by DevicePrefetcher",
-                "h2d_bytes_per_step": B * d0 * 4 + B * 8, "d2h_bytes_per_step": 8 + 4},
+                "path": "LayerTrainer.step fed by DevicePrefetcher (pinned H2D of x, gy one step ahead); y and dx "
+                        "copied to pinned host buffers on a side stream every step",
+                "h2d_bytes_per_step": 2 * B * d * 4, "d2h_bytes_per_step": 2 * B * d * 4},
         "cpu_baseline": cpu,
-        "ukan_layer": ukan,
-        "kan_layers": cfg_rates,
-        "pinn": pinn,
+        **supp,
     }
     print(json.dumps(line), flush=True)
 
 
+def cfg2_rate(dev, steps=20, warmup=5):
+    """Supplementary (the round-1 headline): KAN stack [784, 256, 10], G = 32, batch 8192,
+    softmax-CE + Adam, one full training step captured as a CUDA graph."""
+    import torch
+    import paper_2408_11200_b200 as P
+    from paper_2408_11200_b200 import ops
+    B, widths = 8192, [784, 256, 10]
+    model = P.build_model("kan", widths, 3, seed=0, device=dev, g_min=-1.0, g_max=1.0, G=32)
+    tr = P.SplineTrainer(model, "softmax_cross_entropy", 1e-3, "adam")
+    ops.set_check_mode("deferred")
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    xs = [torch.rand((B, widths[0]), device=dev, generator=g) * 2 - 1 for _ in range(8)]
+    ys = [torch.randint(0, widths[-1], (B,), device=dev, generator=g) for _ in range(8)]
+    for s in range(warmup):
+        tr.step(xs[s % 8], ys[s % 8])
+    tr.read_loss(tr.step(xs[0], ys[0]))
+    cap = tr.capture(xs[0], ys[0])
+    for s in range(3):
+        tr.read_loss(cap.replay(xs[s], ys[s]))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for s in range(steps):
+        loss = cap.replay(xs[s % 8], ys[s % 8])
+    b.record()
+    torch.cuda.synchronize()
+    tr.read_loss(loss)
+    ops.flush_checks()
+    ops.set_check_mode("eager")
+    ms = a.elapsed_time(b) / steps
+    return {"workload": "cfg2: KAN [784,256,10] G=32 k=3 B=8192 softmax-CE + Adam, one training step (CUDA graph)",
+            "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "steps": steps,
+            "l2": "inputs rotate over 8 resident batches (196 MiB > L2)"}
+
+
+def cfg5_rate(dev, world, rank, steps=5, warmup=2):
+    """Supplementary cfg5 (shape proposed): UKAN denoiser-shaped
+    stack [64, 512, 512, 64], delta_g = 0.4, d_pe = d_femb = 24, x ~ N(0, 1), MSE to N(0, 1)
+    targets (epsilon prediction), Adam; GLOBAL batch 65536 sharded over the ranks (strong
+    scaling), gradients all-reduced over NCCL."""
+    import torch
+    import torch.distributed as dist
+    import paper_2408_11200_b200 as P
+    from paper_2408_11200_b200.train import shard_bounds
+    Bg = 65536
+    lo, hi = shard_bounds(Bg, rank, world)
+    Bl = hi - lo
+    model = P.build_model("ukan", [64, 512, 512, 64], 3, seed=0, device=dev, delta_g=0.4, d_pe=24, d_femb=24)
+    tr = P.SplineTrainer(model, "mse", 1e-3, "adam")
+    g = torch.Generator(device=dev)
+    g.manual_seed(5 + rank)
+    x = torch.randn((Bl, 64), device=dev, generator=g)
+    tgt = torch.randn((Bl, 64), device=dev, generator=g)
+    for _ in range(warmup):
+        tr.read_loss(tr.step(x, tgt, n_global=Bg))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        loss = tr.step(x, tgt, n_global=Bg)
+    b.record()
+    torch.cuda.synchronize()
+    tr.read_loss(loss)
+    ms = a.elapsed_time(b) / steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": "cfg5: UKAN [64,512,512,64] k=3 delta_g=0.4 d_pe=d_femb=24, MSE + Adam, global batch 65536 "
+                        f"sharded over {world} GPU(s) ({Bl} per GPU), NCCL all-reduce of the gradients",
+            "samples_per_s": Bg / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "scaling": "strong",
+            "n_gpus": world, "path": "SplineTrainer.step (eager: one host read of the key count per UKAN layer)"}
+
+
 def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
-    """Supplementary UKAN measurement (not the headline): one cfg4-shaped UKAN layer (1024 -> 1024,
-    k=3, delta_g=0.5, d_pe=d_femb=32; x ~ N(0, 20^2)) forward + backward of x and every parameter
-    through the drop-in API (key dedup, CG MLP on the tensor cores, spline kernels), device-timed."""
+    """Supplementary: one cfg4-shaped UKAN layer (1024 -> 1024, k=3, delta_g=0.5,
+    d_pe=d_femb=32; x ~ N(0, 20^2)) forward + backward of x and every parameter through the
+    drop-in API (key dedup, CG MLP, spline kernels), device-timed."""
     import torch
     import paper_2408_11200_b200 as P
     layer = P.init_layer("ukan", 1024, 1024, 3, seed=0, delta_g=0.5, d_pe=32, d_femb=32, device=dev)
@@ -371,48 +500,37 @@ def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
 
 
 def kan_layer_rates(dev):
-    """Supplementary single-layer KAN measurements at BASELINE configs[0] and configs[2] (SURVEY
-    8d D4): forward + backward of every parameter (x is input data: no dx) through the drop-in
-    API, device-timed (CUDA events), with the FP32/FP64 roof fraction of the layer's algorithmic
-    flops (forward 2KBio on FP32, table gradient 2KBio on FP64)."""
+    """Supplementary configs[0] (cfg1: KAN 64 -> 64, G = 10, B = 1024): fwd + parameter grads
+    through the drop-in API, device-timed, with its FP32/FP64 roof fraction."""
     import torch
     import paper_2408_11200_b200 as P
-    out = {}
-    for name, (d, G, B, steps, outl) in {"cfg1": (64, 10, 1024, 50, 0.0), "cfg3": (4096, 64, 65536, 2, 0.01)}.items():
-        layer = P.init_layer("kan", d, d, 3, seed=0, g_min=-1.0, g_max=1.0, G=G, device=dev)
-        g = torch.Generator(device=dev)
-        g.manual_seed(3)
-        x = torch.rand((B, d), device=dev, generator=g) * 2 - 1
-        if outl:
-            m = torch.rand((B, d), device=dev, generator=g) < outl
-            x = torch.where(m, x * 3, x)
-        gy = torch.randn((B, d), device=dev, generator=g)
-        params = [layer.coeffs, layer.scale]
-        for _ in range(2):
-            torch.autograd.grad(P.kan_forward(layer, x), params, gy)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(steps):
-            torch.autograd.grad(P.kan_forward(layer, x), params, gy)
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / steps
-        fl = 2.0 * 4 * B * d * d
-        roof_ms = (fl / (FP32_TFLOPS_MEASURED * 1e12) + fl / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3
-        out[name] = {"workload": f"KAN layer {d}->{d} G={G} k=3 B={B}" + (", 1% clamp tail" if outl else "")
-                     + ", fwd + parameter grads", "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms,
-                     "steps": steps, "roof_ms": roof_ms, "roof_frac": roof_ms / ms}
-        del layer, x, gy
-        torch.cuda.empty_cache()
-    return out
+    d, G, B, steps = 64, 10, 1024, 50
+    layer = P.init_layer("kan", d, d, 3, seed=0, g_min=-1.0, g_max=1.0, G=G, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    x = torch.rand((B, d), device=dev, generator=g) * 2 - 1
+    gy = torch.randn((B, d), device=dev, generator=g)
+    params = [layer.coeffs, layer.scale]
+    for _ in range(3):
+        torch.autograd.grad(P.kan_forward(layer, x), params, gy)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        torch.autograd.grad(P.kan_forward(layer, x), params, gy)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    fl = kan_flops(B, d, d, 3)
+    roof_ms = (fl / (FP32_TFLOPS_MEASURED * 1e12) + fl / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3
+    return {"cfg1": {"workload": "KAN layer 64->64 G=10 k=3 B=1024, fwd + parameter grads (autograd API)",
+                     "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "roof_ms": roof_ms,
+                     "roof_frac": roof_ms / ms}}
 
 
 def pinn_rate(dev, n_colloc=128, steps=50, warmup=5):
-    """Supplementary F2 measurement: one PINN step (pinn_loss through the forward-tangent kernels of
-    a [1, 5, 1] KAN and a [1, 5, 1] UKAN, tasks.py:153-166, plus the reverse pass through the
-    tangent graph), device-timed; tiny and launch-bound by nature."""
-    import numpy as np
+    """Supplementary F2: one PINN step (pinn_loss through the forward-tangent kernels of a
+    [1, 5, 1] KAN and UKAN, tasks.py:153-166, plus the reverse pass), device-timed."""
     import torch
     import paper_2408_11200_b200 as P
     out = {}
@@ -443,8 +561,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-ukan", action="store_true", help="skip the supplementary UKAN layer measurement")
-    ap.add_argument("--no-configs", action="store_true", help="skip the supplementary cfg1 / cfg3 layer measurements")
+    ap.add_argument("--no-configs", action="store_true", help="skip the supplementary cfg1/2/4/5 and PINN fields")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

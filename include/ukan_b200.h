@@ -108,6 +108,20 @@ int ukan_kan_backward_ws2(const float* x, const float* coeffs, const float* scal
                           int64_t d_out, int64_t G, int k, double g_min, double g_max,
                           void* workspace, int64_t workspace_bytes, int flags, void* stream);
 
+/* Feature-sliced backward for data-parallel callers (k = 3, G <= 64, no base branch,
+ * d_out >= 64 and a multiple of 4: ukan_kan_backward_part_supported returns 1).  After
+ * ukan_kan_backward_prep has filled `workspace` for the WHOLE layer (prepared = 1), each call
+ * computes, for features [i_lo, i_hi) only: what & 1 -> dcoeffs / dscale rows of those features
+ * (written), what & 2 -> dx[:, i_lo:i_hi) (written; dx is the full [B, d_in] buffer).  The
+ * slices of one layer are independent, so a caller can all-reduce a finished dcoeffs slice while
+ * the next slice is computed (SURVEY 8e E1 bucketing).  Results equal ukan_kan_backward_ws2
+ * bitwise. */
+int ukan_kan_backward_part_supported(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k);
+int ukan_kan_backward_part(const float* coeffs, const float* scale, const float* gy, float* dx,
+                           float* dcoeffs, float* dscale, int64_t B, int64_t d_in, int64_t d_out,
+                           int64_t G, int k, double g_min, double g_max, void* workspace,
+                           int64_t workspace_bytes, int64_t i_lo, int64_t i_hi, int what, void* stream);
+
 /* Grid location only (for parity tests / tooling): cell [B, d_in] int32 and u [B, d_in]
  * double exactly as layers.py:296-300 compute them. */
 int ukan_kan_locate(const float* x, int32_t* cell, double* u,
@@ -169,10 +183,11 @@ int ukan_ukan_build_keys(const float* x, int64_t B, int64_t d_in, int k, double 
                          int64_t* n_unique_host, int64_t* max_rows_host,
                          int32_t* nonfinite_host, void* stream);
 
-/* Coefficient-generator input rows: inp[n_u, d_femb + d_pe] = [emb[f] || PE(group)] with the
- * PE evaluated in fp64 (layers.py:112-123, 238-240). */
+/* Coefficient-generator input rows: inp[n_u, d_femb + d_pe] = [emb[f] || PE(group)] in fp64
+ * (the PE evaluated and KEPT in fp64 as the reference does, layers.py:112-123, 238-240; the
+ * embedding is widened exactly).  The whole CG chain stays fp64 between its GEMMs. */
 int ukan_ukan_cg_input(const int32_t* key_f, const int64_t* key_g, const float* emb,
-                       float* inp, int64_t n_u, int64_t d_femb, int64_t d_pe, void* stream);
+                       double* inp, int64_t n_u, int64_t d_femb, int64_t d_pe, void* stream);
 
 /* Dense row-major GEMM family used by the CG MLP (layers.py:241-242, tensor.py:189-197):
  *   C[M,N] = act(A[M,K] @ B[K,N] + bias[N])         (ukan_gemm_bias_act, act 0=none 1=silu,
@@ -187,13 +202,34 @@ int ukan_gemm_nt(const float* A, const float* Bm, float* C, int64_t M, int64_t N
 int ukan_gemm_tn(const float* A, const float* Bm, float* C, float* colsum_B,
                  int64_t M, int64_t N, int64_t K, void* stream);
 
-/* d(silu): dpre = dH * (s + pre*s*(1-s)), s = sigmoid(pre)  (tensor.py:232-233). */
-int ukan_silu_backward(const float* pre, const float* dH, float* dpre, int64_t n, void* stream);
+/* Diagnostic, not used by the product path: C[M,N] = A[K,M]^T @ B[K,N] on the tcgen05 tensor
+ * cores in the 3xTF32 form SURVEY 8c C5 proposed for the CG gradient GEMMs (round-to-nearest
+ * tf32 operand splits, fp64 promotion per 32-wide K chunk, split-K over 4096 rows summed in
+ * fp64).  Kept so tests can measure why ukan_gemm_tn runs on FP64 DMMA instead (the fp32 tensor
+ * core accumulator keeps ~22 bits).  M, N multiples of 4; A, B 16-byte aligned. */
+int ukan_gemm_tn_tf32x3_probe(const float* A, const float* Bm, float* C, int64_t M, int64_t N,
+                              int64_t K, void* stream);
+
+/* d(silu): dpre = dH * (s + pre*s*(1-s)), s = sigmoid(pre)  (tensor.py:232-233), fp64. */
+int ukan_silu_backward(const double* pre, const double* dH, double* dpre, int64_t n, void* stream);
+
+/* GEMM on the FP64 tensor cores (mma.sync m8n8k4 f64, fp64 products and sums, split-K partials
+ * reduced in fixed order) with fp32 or fp64 operands (dtype UKAN_F32 / UKAN_F64, widened exactly):
+ *   op 0 (NN): A [M,K], B [K,N];  op 1 (NT): A [M,K], B [N,K];  op 2 (TN): A [K,M], B [K,N].
+ * Epilogue in fp64: v = A.B + bias[n] (bias nullable); pre_out = v; v = silu(v) if act;
+ * C64 = v; C32 = (float)v (each output nullable, at least one given).  colsum_B (op 2 only,
+ * nullable) = column sums of B in fp64 (the bias gradient of a TN weight-gradient GEMM).
+ * Used for the CG MLP (layers.py:241-242, tensor.py:189-197) in fp64. */
+#define UKAN_F32 0
+#define UKAN_F64 1
+int ukan_gemm_f64(int op, const void* A, int a_dtype, const void* Bm, int b_dtype, const float* bias,
+                  int act, double* pre_out, float* C32, double* C64, float* colsum_B, int64_t M,
+                  int64_t N, int64_t K, void* stream);
 
 /* Embedding gradient: d_emb[f, :] = sum over the rows of feature f (seg_start[f] ..
- * seg_start[f+1]) of dinp[r, :d_femb] (gather_rows bwd, tensor.py:265-268), fp64 sum in key
- * order (deterministic). */
-int ukan_ukan_emb_backward(const int32_t* seg_start, const float* dinp, float* d_emb,
+ * seg_start[f+1]) of dinp[r, :d_femb] (gather_rows bwd, tensor.py:265-268; dinp fp64), fp64 sum
+ * in key order (deterministic). */
+int ukan_ukan_emb_backward(const int32_t* seg_start, const double* dinp, float* d_emb,
                            int64_t d_in, int64_t d_femb, int64_t d_cg_in, void* stream);
 
 /* UKAN spline forward over the generated table: table [n_u*K, d_out] (slot-major view of the
@@ -233,10 +269,13 @@ int ukan_ukan_jvp_backward(const float* x, const float* tx, const int32_t* base_
 
 /* Mean softmax cross-entropy over logits [n, c] and int64 labels [n] (tensor.py:377-400):
  * loss points at 1 + n device doubles; loss[0] = sum of this shard's row losses / n_global
- * (loss[1..n] is per-row scratch); dlogits = grad_scale * (softmax - onehot) / n_global. */
+ * (loss[1..n] is per-row scratch); dlogits = grad_scale * (softmax - onehot) / n_global.
+ * A label outside [0, c) is never dereferenced: its row loss is NaN, its gradient row 0, and
+ * bit 1 (value 2) is OR-ed into *err_flag (device int32, nullable) so the caller can raise the
+ * reference's IndexError (tensor.py:388-392) at its next host read. */
 int ukan_softmax_xent(const float* logits, const int64_t* labels, double* loss,
                       float* dlogits, int64_t n, int64_t c, int64_t n_global,
-                      double grad_scale, void* stream);
+                      double grad_scale, int32_t* err_flag, void* stream);
 
 /* Mean squared error over pred/target [n] elements (tensor.py:368-374): loss points at
  * 1 + n device doubles, loss[0] = sum (pred-target)^2 / n_global; dpred = 2*(pred-target)/n_global. */
@@ -254,8 +293,9 @@ int ukan_adam_step(float* p, const float* g, float* m, float* v, int64_t n, doub
                    const double* guard, void* stream);
 
 /* SGD step p -= lr*g (optim.py:18-21), same guard semantics. */
-/* Graph-replayable Adam (for a step captured as a CUDA graph): increments the device step
- * counter *t, computes the bias corrections 1 - beta^t into bc[2] (device), reads the learning
+/* Graph-replayable Adam (for a step captured as a CUDA graph): unless *guard is non-finite
+ * (skipped step, counter unchanged, as the reference raises before state.t += 1) increments the
+ * device step counter *t, computes the bias corrections 1 - beta^t into bc[2] (device), reads the learning
  * rate from *lr (device) and updates as ukan_adam_step.  All of t, bc, lr are device pointers. */
 int ukan_adam_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const double* lr,
                        double beta1, double beta2, double eps, double weight_decay, int64_t* t,

@@ -13,6 +13,7 @@ produced by the reference implementation itself (``tests/golden/make_golden.py``
 from .spline import (basis_matrix, basis_values, kan_locate, kan_forward_backward,
                      ukan_locate, ukan_keys, positional_encoding, cg_forward,
                      ukan_forward_backward, kan_tangent_forward_backward,
-                     ukan_tangent_forward_backward, softmax_xent, mse, adam_step, model_step)
+                     ukan_tangent_forward_backward, softmax_xent, mse, adam_step, model_step,
+                     kan_rows, kan_feature_grads)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -356,3 +356,55 @@ def model_step(kind, layer_params, layer_cfgs, x, target, loss_kind, lr, t=1, we
     new_p = [a.copy() for a in flat_p]
     adam_step(new_p, flat_g, m, v, t, lr, weight_decay=weight_decay)
     return loss, grads, new_p, m, v
+
+
+# ---------------------------------------------------------------------------------------
+# Memory-bounded forms for parity at the benchmarked (full) shapes.  The reference
+# materialises windows [B, d_in, K, d_out] (layers.py:65) and a full zeros_like(table)
+# (layers.py:68), which is 35 PB at cfg3; the two functions below compute the SAME float64
+# quantities on a subset: per-sample rows (y, dx of a few samples need only those samples) and
+# per-feature gradients (dC[i], dscale[i] need only column i of x and the whole upstream g).
+# Only the float64 summation order differs from the reference (~1e-16 relative).
+# ---------------------------------------------------------------------------------------
+def kan_rows(x_rows, coeffs, scale, gy_rows, *, k, g_min, g_max, G, feat_block=256):
+    """y and dx of the given sample rows (layers.py:304-318 forward; basis_features /
+    edge_combine / clamp bwd, layers.py:44-46, 84-88, tensor.py:327-338), features in blocks so
+    the windows of one block stay small.  Returns dict(y [n, d_out], dx [n, d_in], cell)."""
+    x_rows = np.asarray(x_rows, dtype=np.float64)
+    n, f = x_rows.shape
+    y = np.zeros((n, coeffs.shape[2]))
+    dx = np.zeros((n, f))
+    cells = np.zeros((n, f), dtype=np.int64)
+    for i0 in range(0, f, feat_block):
+        sl = slice(i0, min(f, i0 + feat_block))
+        K = k + 1
+        cell, u, mask = kan_locate(x_rows[:, sl], g_min, g_max, G)
+        cells[:, sl] = cell
+        fi = np.arange(sl.start, sl.stop)
+        win = coeffs[fi[None, :, None], cell[..., None] + np.arange(K)]        # layers.py:65
+        basis = basis_values(u, k)
+        tmp = np.einsum("bfj,bfjo->bfo", basis, win)                           # layers.py:81
+        y += np.einsum("bfo,fo->bo", tmp, scale[sl])                           # layers.py:82
+        dtmp = gy_rows[:, None, :] * scale[None, sl, :]                        # layers.py:85
+        dbasis = np.einsum("bfo,bfjo->bfj", dtmp, win)                         # layers.py:87
+        du = (dbasis * basis_values(u, k, 1)).sum(axis=-1)                     # layers.py:44-46
+        dx[:, sl] = du * (1.0 / ((g_max - g_min) / G)) * mask
+    return dict(y=y, dx=dx, cell=cells)
+
+
+def kan_feature_grads(x_col, coeffs_i, scale_i, gy, *, k, g_min, g_max, G):
+    """dC[i] [G+k, d_out] and dscale[i] [d_out] of ONE feature over the whole batch: the
+    np.add.at scatter of layers.py:67-70 written as the equivalent dense product
+    W[r, b] @ g[b, o] with W[c_b + j, b] = w_j(u_b) (float64), then edge_combine's bwd
+    (layers.py:84-88): dC = scale * A, dscale = sum_b g * tmp = sum_r C * A."""
+    x_col = np.asarray(x_col, dtype=np.float64)
+    B = x_col.shape[0]
+    K = k + 1
+    R = G + k
+    cell, u, _ = kan_locate(x_col, g_min, g_max, G)
+    basis = basis_values(u, k)                                                  # [B, K]
+    W = np.zeros((R, B))
+    for j in range(K):
+        W[cell + j, np.arange(B)] = basis[:, j]
+    A = W @ np.asarray(gy, dtype=np.float64)                                    # [R, d_out]
+    return dict(dcoeffs=scale_i[None, :] * A, dscale=(coeffs_i * A).sum(axis=0))

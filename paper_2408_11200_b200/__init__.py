@@ -11,7 +11,7 @@ from .layers import (KanLayer, LinearLayer, Model, UkanLayer, build_model, cg_co
 from .optim import AdamState, LrSchedule, adam_step, lr_at, sgd_step
 from .ops import flush_checks, set_check_mode
 from .pinn import PinnProblem, pinn_loss
-from .train import CapturedStep, DevicePrefetcher, GradSync, SplineTrainer, shard_bounds
+from .train import CapturedStep, DevicePrefetcher, GradSync, LayerTrainer, SplineTrainer, shard_bounds
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"

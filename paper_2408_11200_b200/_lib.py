@@ -22,6 +22,8 @@ UKAN_E_DEGREE = -2
 UKAN_E_GRID = -3
 UKAN_E_WORKSPACE = -4
 UKAN_E_CAPACITY = -5
+UKAN_F32 = 0
+UKAN_F64 = 1
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -46,6 +48,9 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_kan_backward_ws2": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64,
                                      _P, _I64, _INT, _P]),
     "ukan_kan_backward_prep": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _I64, _P, _P]),
+    "ukan_kan_backward_part_supported": (_INT, [_I64, _I64, _I64, _I64, _INT]),
+    "ukan_kan_backward_part": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P, _I64,
+                                      _I64, _I64, _INT, _P]),
     "ukan_kan_naive_forward": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),
     "ukan_kan_naive_backward": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),
     "ukan_kan_jvp_forward": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _F64, _P]),
@@ -63,13 +68,15 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_gemm_bias_act": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _INT, _P]),
     "ukan_gemm_nt": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "ukan_gemm_tn": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _P]),
+    "ukan_gemm_tn_tf32x3_probe": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "ukan_silu_backward": (_INT, [_P, _P, _P, _I64, _P]),
+    "ukan_gemm_f64": (_INT, [_INT, _P, _INT, _P, _INT, _P, _INT, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
     "ukan_ukan_emb_backward": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "ukan_ukan_forward": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _INT, _F64, _P]),
     "ukan_ukan_backward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),
     "ukan_ukan_backward": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64,
                                   _P, _I64, _P]),
-    "ukan_softmax_xent": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _F64, _P]),
+    "ukan_softmax_xent": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _P]),
     "ukan_mse": (_INT, [_P, _P, _P, _P, _I64, _I64, _P]),
     "ukan_adam_step": (_INT, [_P, _P, _P, _P, _I64, _F64, _F64, _F64, _F64, _F64, _I64, _P, _P]),
     "ukan_sgd_step": (_INT, [_P, _P, _I64, _F64, _P, _P]),
@@ -104,6 +111,17 @@ def require_cuda(*tensors: torch.Tensor) -> None:
     for t in tensors:
         if t is not None and not t.is_cuda:
             raise RuntimeError("all tensors must live on the CUDA device")
+
+
+def require_params(device, *params: torch.Tensor | None) -> None:
+    """Layer parameters go to the kernels as raw pointers: they must be fp32, contiguous and on
+    the input's device (a float64 or strided tensor would be read as garbage)."""
+    for t in params:
+        if t is None:
+            continue
+        if t.dtype != torch.float32 or not t.is_contiguous() or t.device != device:
+            raise ConfigError(f"layer parameters must be contiguous float32 tensors on {device}; got "
+                              f"{t.dtype}, contiguous={t.is_contiguous()}, device={t.device}")
 
 
 def ptr(t: torch.Tensor | None):

@@ -23,6 +23,7 @@ int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_
                int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
                int S, int64_t kps, cudaStream_t st);
 int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st);
+int cg_colsum64(const double* X, float* out, int64_t K, int64_t N, cudaStream_t st);
 // fp64 tensor-core gradient GEMMs (cg_dmma.cu)
 int64_t cg_dmma_workspace(int64_t M, int64_t N, int64_t K);
 int cg_dmma_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
@@ -47,20 +48,20 @@ struct PeFreqs {
 
 __global__ void cg_input_kernel(const int32_t* __restrict__ key_f,
                                 const int64_t* __restrict__ key_g, const float* __restrict__ emb,
-                                float* __restrict__ inp, int64_t n_u, int d_femb, int d_pe,
+                                double* __restrict__ inp, int64_t n_u, int d_femb, int d_pe,
                                 PeFreqs fr) {
   const int W = d_femb + d_pe;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_u * W) return;
   const int64_t r = t / W;
   const int c = (int)(t % W);
-  float v;
+  double v;
   if (c < d_femb) {
-    v = emb[(size_t)key_f[r] * d_femb + c];
-  } else {
+    v = (double)emb[(size_t)key_f[r] * d_femb + c];
+  } else {  // fp64 PE kept in fp64: rounding it to fp32 alone costs 1.5x the CG-gradient tolerance
     const int m = (c - d_femb) >> 1;
     const double ang = (double)key_g[r] * fr.f[m];  // g[..., None] * freqs  (layers.py:119)
-    v = (float)(((c - d_femb) & 1) ? cos(ang) : sin(ang));
+    v = ((c - d_femb) & 1) ? cos(ang) : sin(ang);
   }
   inp[t] = v;
 }
@@ -126,22 +127,22 @@ gemm_nn_kernel(const float* __restrict__ A, const float* __restrict__ Bm,
 
 
 
-__global__ void silu_bwd_kernel(const float* __restrict__ pre, const float* __restrict__ dH,
-                                float* __restrict__ dpre, int64_t n) {
+__global__ void silu_bwd_kernel(const double* __restrict__ pre, const double* __restrict__ dH,
+                                double* __restrict__ dpre, int64_t n) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  dpre[t] = (float)((double)dH[t] * dsilu_d((double)pre[t]));
+  dpre[t] = dH[t] * dsilu_d(pre[t]);
 }
 
 // d_emb[f, c] = sum_{r in seg(f)} dinp[r, c], c < d_femb, fp64, key order.
 __global__ void emb_bwd_kernel(const int32_t* __restrict__ seg_start,
-                               const float* __restrict__ dinp, float* __restrict__ d_emb,
+                               const double* __restrict__ dinp, float* __restrict__ d_emb,
                                int d_in, int d_femb, int d_cg_in) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)d_in * d_femb) return;
   const int f = (int)(t / d_femb), c = (int)(t % d_femb);
   double s = 0.0;
-  for (int r = seg_start[f]; r < seg_start[f + 1]; ++r) s += (double)dinp[(size_t)r * d_cg_in + c];
+  for (int r = seg_start[f]; r < seg_start[f + 1]; ++r) s += dinp[(size_t)r * d_cg_in + c];
   d_emb[t] = (float)s;
 }
 
@@ -150,7 +151,7 @@ __global__ void emb_bwd_kernel(const int32_t* __restrict__ seg_start,
 using namespace ukan;
 
 extern "C" int ukan_ukan_cg_input(const int32_t* key_f, const int64_t* key_g, const float* emb,
-                                  float* inp, int64_t n_u, int64_t d_femb, int64_t d_pe,
+                                  double* inp, int64_t n_u, int64_t d_femb, int64_t d_pe,
                                   void* stream) {
   if (d_pe % 2 != 0 || d_pe / 2 > kMaxPeHalf || d_femb < 0 || n_u < 0) return UKAN_E_ARG;
   if (n_u == 0) return UKAN_OK;
@@ -201,7 +202,7 @@ extern "C" int ukan_gemm_tn(const float* A, const float* Bm, float* C, float* co
   return colsum_B ? cg_colsum(Bm, colsum_B, K, N, st) : UKAN_OK;
 }
 
-extern "C" int ukan_silu_backward(const float* pre, const float* dH, float* dpre, int64_t n,
+extern "C" int ukan_silu_backward(const double* pre, const double* dH, double* dpre, int64_t n,
                                   void* stream) {
   if (n < 0 || !pre || !dH || !dpre) return UKAN_E_ARG;
   if (n == 0) return UKAN_OK;
@@ -210,7 +211,7 @@ extern "C" int ukan_silu_backward(const float* pre, const float* dH, float* dpre
   return UKAN_OK;
 }
 
-extern "C" int ukan_ukan_emb_backward(const int32_t* seg_start, const float* dinp, float* d_emb,
+extern "C" int ukan_ukan_emb_backward(const int32_t* seg_start, const double* dinp, float* d_emb,
                                       int64_t d_in, int64_t d_femb, int64_t d_cg_in,
                                       void* stream) {
   if (d_in < 1 || d_femb < 0 || d_cg_in < d_femb || !seg_start || !d_emb) return UKAN_E_ARG;
@@ -220,4 +221,44 @@ extern "C" int ukan_ukan_emb_backward(const int32_t* seg_start, const float* din
       seg_start, dinp, d_emb, (int)d_in, (int)d_femb, (int)d_cg_in);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
+}
+
+// Mixed-precision GEMM on the FP64 tensor cores (cg_dmma.cu) for the fp64 CG chain.
+extern "C" int ukan_gemm_f64(int op, const void* A, int a_dtype, const void* Bm, int b_dtype, const float* bias,
+                             int act, double* pre_out, float* C32, double* C64, float* colsum_B, int64_t M, int64_t N,
+                             int64_t K, void* stream) {
+  if (M < 0 || N < 1 || K < 0 || M > INT32_MAX || K > INT32_MAX || !A || !Bm || (!C32 && !C64 && !pre_out))
+    return UKAN_E_ARG;
+  if (op < 0 || op > 2 || (a_dtype != UKAN_F32 && a_dtype != UKAN_F64) || (b_dtype != UKAN_F32 && b_dtype != UKAN_F64))
+    return UKAN_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M == 0) return UKAN_OK;
+  DgOut o;
+  o.c32 = C32;
+  o.c64 = C64;
+  o.pre64 = pre_out;
+  o.bias = bias;
+  o.act = act;
+  // strides: NN A [M,K] B [K,N]; NT A [M,K] B [N,K]; TN A [K,M] B [K,N]
+  const int64_t sam = op == 2 ? 1 : K, sak = op == 2 ? M : 1;
+  const int64_t sbk = op == 1 ? 1 : N, sbn = op == 1 ? K : 1;
+  if (K == 0) return UKAN_E_ARG;
+  const int64_t nb = cg_dmma_workspace(M, N, K);
+  void* part = nullptr;
+  if (nb > 0) UKAN_CUDA_TRY(scratch_alloc(&part, (size_t)nb, st));
+  double* pd = static_cast<double*>(part);
+  int rc;
+  if (a_dtype == UKAN_F32 && b_dtype == UKAN_F32)
+    rc = cg_dmma_gemm_t<float, float>((const float*)A, sam, sak, (const float*)Bm, sbk, sbn, M, N, K, o, pd, st);
+  else if (a_dtype == UKAN_F64 && b_dtype == UKAN_F32)
+    rc = cg_dmma_gemm_t<double, float>((const double*)A, sam, sak, (const float*)Bm, sbk, sbn, M, N, K, o, pd, st);
+  else if (a_dtype == UKAN_F32)
+    rc = cg_dmma_gemm_t<float, double>((const float*)A, sam, sak, (const double*)Bm, sbk, sbn, M, N, K, o, pd, st);
+  else
+    rc = cg_dmma_gemm_t<double, double>((const double*)A, sam, sak, (const double*)Bm, sbk, sbn, M, N, K, o, pd, st);
+  if (part) cudaFreeAsync(part, st);
+  if (rc || !colsum_B) return rc;
+  if (op != 2) return UKAN_E_ARG;  // column sums of B (the bias gradient) belong to the TN form
+  return b_dtype == UKAN_F32 ? cg_colsum((const float*)Bm, colsum_B, K, N, st)
+                             : cg_colsum64((const double*)Bm, colsum_B, K, N, st);
 }

@@ -29,11 +29,21 @@ __device__ __forceinline__ void dg_dmma(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-// D[m, n] = sum_k A(m,k) B(k,n) with A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn];
-// out = C (fp32) when part == nullptr, else part[z][m][n] (fp64 partial of K-slice z).
+__device__ __forceinline__ void dg_epilogue(const DgOut& o, int64_t idx, int n, double v) {
+  if (o.bias) v += (double)o.bias[n];
+  if (o.pre64) o.pre64[idx] = v;
+  if (o.act) v = silu_d(v);
+  if (o.c64) o.c64[idx] = v;
+  if (o.c32) o.c32[idx] = (float)v;
+}
+
+// D[m, n] = sum_k A(m,k) B(k,n) with A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn]; TA / TB
+// are float (widened exactly when staged) or double.  part == nullptr: epilogue `out`; else
+// part[z][m][n] (fp64 partial of K-slice z).
+template <typename TA, typename TB>
 __global__ void __launch_bounds__(kDgThreads, 1)
-cg_dmma_gemm_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const float* __restrict__ Bm, int64_t sbk,
-                    int64_t sbn, int M, int N, int K, int kps, float* __restrict__ C, double* __restrict__ part) {
+cg_dmma_gemm_kernel(const TA* __restrict__ A, int64_t sam, int64_t sak, const TB* __restrict__ Bm, int64_t sbk,
+                    int64_t sbn, int M, int N, int K, int kps, DgOut out, double* __restrict__ part) {
   extern __shared__ __align__(16) double dsm[];
   double* As = dsm;                          // 2 x [kDgM][kDgAS]
   double* Bs = dsm + 2 * kDgM * kDgAS;       // 2 x [kDgK][kDgBS]
@@ -46,7 +56,8 @@ cg_dmma_gemm_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const
   const int nch = (ke - kb + kDgK - 1) / kDgK;
 
   // staging registers: A chunk 128 x 32 = 16 / thread, B chunk 32 x 64 = 8 / thread
-  float ra[16], rb[8];
+  TA ra[16];
+  TB rb[8];
   auto fetch = [&](int c) {
     const int k0 = kb + c * kDgK;
 #pragma unroll
@@ -55,7 +66,7 @@ cg_dmma_gemm_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const
       int m, k;
       if (sak == 1) { m = e >> 5; k = e & 31; } else { k = e >> 7; m = e & 127; }  // walk the contiguous dim
       const int gm = m0 + m, gk = k0 + k;
-      ra[q] = (gm < M && gk < ke) ? __ldg(A + (size_t)gm * sam + (size_t)gk * sak) : 0.f;
+      ra[q] = (gm < M && gk < ke) ? __ldg(A + (size_t)gm * sam + (size_t)gk * sak) : (TA)0;
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -63,7 +74,7 @@ cg_dmma_gemm_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const
       int n, k;
       if (sbk == 1) { n = e >> 5; k = e & 31; } else { k = e >> 6; n = e & 63; }
       const int gn = n0 + n, gk = k0 + k;
-      rb[q] = (gn < N && gk < ke) ? __ldg(Bm + (size_t)gk * sbk + (size_t)gn * sbn) : 0.f;
+      rb[q] = (gn < N && gk < ke) ? __ldg(Bm + (size_t)gk * sbk + (size_t)gn * sbn) : (TB)0;
     }
   };
   auto store = [&](int buf) {  // exact fp32 -> fp64 widening
@@ -125,18 +136,18 @@ cg_dmma_gemm_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const
         const int m = m0 + wm + i * 8 + grp, n = n0 + wn + j * 8 + 2 * kq + v;
         if (m < M && n < N) {
           if (part) part[((size_t)z * M + m) * N + n] = acc[i][j][v];
-          else C[(size_t)m * N + n] = (float)acc[i][j][v];
+          else dg_epilogue(out, (int64_t)m * N + n, n, acc[i][j][v]);
         }
       }
 }
 
-// C[m][n] = sum_z part[z][m][n] (fp64, fixed order).
-__global__ void cg_dmma_reduce_kernel(const double* __restrict__ part, float* __restrict__ C, int64_t MN, int S) {
+// out[m][n] = epilogue(sum_z part[z][m][n]) (fp64, fixed order).
+__global__ void cg_dmma_reduce_kernel(const double* __restrict__ part, DgOut out, int64_t MN, int N, int S) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= MN) return;
   double a = 0.0;
   for (int z = 0; z < S; ++z) a += part[(size_t)z * MN + t];
-  C[t] = (float)a;
+  dg_epilogue(out, t, (int)(t % N), a);
 }
 
 int kan_num_sms();
@@ -154,25 +165,42 @@ int64_t cg_dmma_workspace(int64_t M, int64_t N, int64_t K) {
   return S > 1 ? (int64_t)sizeof(double) * S * M * N : 0;
 }
 
-int cg_dmma_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
-                 int64_t N, int64_t K, float* C, double* part, cudaStream_t st) {
+template <typename TA, typename TB>
+int cg_dmma_gemm_t(const TA* A, int64_t sam, int64_t sak, const TB* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                   int64_t N, int64_t K, const DgOut& out, double* part, cudaStream_t st) {
   if (M < 1 || N < 1 || K < 1 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return UKAN_E_ARG;
   const int S = dg_splits(M, N, K);
   if (S > 1 && part == nullptr) return UKAN_E_WORKSPACE;
   const int kps = (int)((K + S - 1) / S + kDgK - 1) / kDgK * kDgK;
   const int Sz = (int)((K + kps - 1) / kps);
   const size_t smem = sizeof(double) * 2 * ((size_t)kDgM * kDgAS + (size_t)kDgK * kDgBS);
-  UKAN_CUDA_TRY(cudaFuncSetAttribute(cg_dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = cg_dmma_gemm_kernel<TA, TB>;
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 g((unsigned)((M + kDgM - 1) / kDgM), (unsigned)((N + kDgN - 1) / kDgN), Sz);
-  cg_dmma_gemm_kernel<<<g, kDgThreads, smem, st>>>(A, sam, sak, Bm, sbk, sbn, (int)M, (int)N, (int)K, kps, C,
-                                                   Sz > 1 ? part : nullptr);
+  kern<<<g, kDgThreads, smem, st>>>(A, sam, sak, Bm, sbk, sbn, (int)M, (int)N, (int)K, kps, out,
+                                    Sz > 1 ? part : nullptr);
   UKAN_LAUNCH_CHECK();
   if (Sz > 1) {
     const int64_t MN = M * N;
-    cg_dmma_reduce_kernel<<<(unsigned)((MN + 255) / 256), 256, 0, st>>>(part, C, MN, Sz);
+    cg_dmma_reduce_kernel<<<(unsigned)((MN + 255) / 256), 256, 0, st>>>(part, out, MN, (int)N, Sz);
     UKAN_LAUNCH_CHECK();
   }
   return UKAN_OK;
+}
+template int cg_dmma_gemm_t<float, float>(const float*, int64_t, int64_t, const float*, int64_t, int64_t, int64_t,
+                                          int64_t, int64_t, const DgOut&, double*, cudaStream_t);
+template int cg_dmma_gemm_t<double, float>(const double*, int64_t, int64_t, const float*, int64_t, int64_t, int64_t,
+                                           int64_t, int64_t, const DgOut&, double*, cudaStream_t);
+template int cg_dmma_gemm_t<float, double>(const float*, int64_t, int64_t, const double*, int64_t, int64_t, int64_t,
+                                           int64_t, int64_t, const DgOut&, double*, cudaStream_t);
+template int cg_dmma_gemm_t<double, double>(const double*, int64_t, int64_t, const double*, int64_t, int64_t, int64_t,
+                                            int64_t, int64_t, const DgOut&, double*, cudaStream_t);
+
+int cg_dmma_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                 int64_t N, int64_t K, float* C, double* part, cudaStream_t st) {
+  DgOut o;
+  o.c32 = C;
+  return cg_dmma_gemm_t<float, float>(A, sam, sak, Bm, sbk, sbn, M, N, K, o, part, st);
 }
 
 }  // namespace ukan

@@ -315,7 +315,8 @@ cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const f
 // colsum[n] = sum_k X[k][n] (fp64, fixed order): pass 1 sums 32 columns x one row slice per CTA
 // (8 warps, rows interleaved, then the 8 warp sums in order) into part[slice][n]; pass 2 adds the
 // slices in order.
-__global__ void __launch_bounds__(256) cg_colsum_part_kernel(const float* __restrict__ X, double* __restrict__ part,
+template <typename T>
+__global__ void __launch_bounds__(256) cg_colsum_part_kernel(const T* __restrict__ X, double* __restrict__ part,
                                                              int K, int N, int rows_per_slice) {
   __shared__ double red[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), ty = threadIdx.x >> 5;
@@ -426,7 +427,21 @@ int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st)
   if (v4)
     cg_colsum_part4_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
   else
-    cg_colsum_part_kernel<<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
+    cg_colsum_part_kernel<float><<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
+  UKAN_LAUNCH_CHECK();
+  cg_colsum_final_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(static_cast<double*>(part), out, (int)N, S);
+  UKAN_LAUNCH_CHECK();
+  cudaFreeAsync(part, st);
+  return UKAN_OK;
+}
+
+int cg_colsum64(const double* X, float* out, int64_t K, int64_t N, cudaStream_t st) {
+  const int64_t cblk = (N + 31) / 32;
+  const int S = (int)std::max<int64_t>(1, std::min<int64_t>((4 * kan_num_sms() + cblk - 1) / cblk, (K + 255) / 256));
+  const int rps = (int)((K + S - 1) / S);
+  void* part = nullptr;
+  UKAN_CUDA_TRY(scratch_alloc(&part, sizeof(double) * S * N, st));
+  cg_colsum_part_kernel<double><<<dim3((unsigned)cblk, S), 256, 0, st>>>(X, static_cast<double*>(part), (int)K, (int)N, rps);
   UKAN_LAUNCH_CHECK();
   cg_colsum_final_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(static_cast<double*>(part), out, (int)N, S);
   UKAN_LAUNCH_CHECK();
@@ -435,3 +450,44 @@ int cg_colsum(const float* X, float* out, int64_t K, int64_t N, cudaStream_t st)
 }
 
 }  // namespace ukan
+
+// ---------------------------------------------------------------------------------------
+// Diagnostic (not on the product path): the weight-gradient GEMM C = A^T B (A [K,M], B [K,N])
+// in the form SURVEY 8c C5 proposed for the CG gradients — tcgen05 kind::tf32 with 3-piece
+// round-to-nearest operand splits (6 products), fp64 register promotion of every 32-wide K chunk,
+// split-K over 4096-row slices with the fp32 slice results summed in fp64.  The product path runs
+// these GEMMs on FP64 DMMA instead (cg_dmma.cu); tests/test_cg_tc.py measures both against an fp64
+// reference on a K = 70k reduction to pin why (the tensor core's fp32 accumulator keeps ~22 bits).
+// ---------------------------------------------------------------------------------------
+namespace ukan {
+__global__ void cg_probe_reduce_kernel(const float* __restrict__ part, float* __restrict__ C, int64_t MN, int S) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= MN) return;
+  double s = 0.0;
+  for (int z = 0; z < S; ++z) s += (double)part[(size_t)z * MN + t];
+  C[t] = (float)s;
+}
+}  // namespace ukan
+
+extern "C" int ukan_gemm_tn_tf32x3_probe(const float* A, const float* Bm, float* C, int64_t M, int64_t N, int64_t K,
+                                         void* stream) {
+  using namespace ukan;
+  if (M < 1 || N < 1 || K < 1 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || !A || !Bm || !C) return UKAN_E_ARG;
+  if (M % 4 || N % 4 || ((uintptr_t)A % 16) || ((uintptr_t)Bm % 16)) return UKAN_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t kps = 4096;
+  const int S = (int)((K + kps - 1) / kps);
+  void* part = nullptr;
+  UKAN_CUDA_TRY(scratch_alloc(&part, sizeof(float) * (size_t)S * M * N, st));
+  // A(m, k) = A[k*M + m] (sam = 1, sak = M); B(k, n) = B[k*N + n]
+  int rc = N > 64 ? cg_launch<128, double, 3>(A, 1, M, Bm, N, 1, (int)M, (int)N, (int)K, (int)kps, S, 2, nullptr, 0,
+                                              nullptr, nullptr, static_cast<float*>(part), st)
+                  : cg_launch<64, double, 3>(A, 1, M, Bm, N, 1, (int)M, (int)N, (int)K, (int)kps, S, 2, nullptr, 0,
+                                             nullptr, nullptr, static_cast<float*>(part), st);
+  if (rc == UKAN_OK) {
+    cg_probe_reduce_kernel<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(static_cast<float*>(part), C, M * N, S);
+    UKAN_LAUNCH_CHECK();
+  }
+  cudaFreeAsync(part, st);
+  return rc;
+}

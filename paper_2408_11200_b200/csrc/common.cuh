@@ -32,6 +32,20 @@ namespace ukan {
 // calls do not remap pages at every synchronisation.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 
+// Epilogue of the FP64 tensor-core GEMMs (cg_dmma.cu): v = D + bias[n]; pre64 = v;
+// v = silu(v) if act; c64 = v; c32 = (float)v.  Every pointer is optional; fp64 arithmetic.
+struct DgOut {
+  float* c32 = nullptr;
+  double* c64 = nullptr;
+  double* pre64 = nullptr;
+  const float* bias = nullptr;
+  int act = 0;
+};
+template <typename TA, typename TB>
+int cg_dmma_gemm_t(const TA* A, int64_t sam, int64_t sak, const TB* Bm, int64_t sbk, int64_t sbn, int64_t M,
+                   int64_t N, int64_t K, const DgOut& out, double* part, cudaStream_t st);
+int64_t cg_dmma_workspace(int64_t M, int64_t N, int64_t K);
+
 constexpr int kMaxK = UKAN_MAX_DEGREE + 1;
 
 // Basis matrix passed by value as a kernel parameter (<= 11*11 doubles).

@@ -6,9 +6,9 @@
 //   dC = scale * A,   dscale = sum_r C * A.
 //
 // Two kernels.
-//  * prep: once per (feature, 128-sample chunk) — fp64 locate with the reference's expression
+//  * prep: once per (feature, 256-sample chunk) — fp64 locate with the reference's expression
 //    order (layers.py:299-300), stable counting sort of the chunk by cell, record
-//    {(cell<<8)|sample, u} in cell order plus the start of every cell.  The records of a layer
+//    {(cell<<8)|sample|clamped<<30, u} in cell order plus the start of every cell.  The records of a layer
 //    (~14 B per (sample, feature)) stay L2-resident and are shared by every output tile.
 //  * sweep: a CTA owns 8 features x 8*NT outputs; per chunk it stages (cp.async, double
 //    buffered) the 8 feature records and g[chunk, o-tile].  Rows are covered by 8-row blocks
@@ -30,6 +30,7 @@
 namespace ukan {
 
 constexpr int kTcBC = 256;  // samples per chunk (the sample index is packed in 8 bits)
+constexpr int kTcClamped = 1 << 30;  // record flag: x outside [g_min, hi] (clamp mask 0, tensor.py:330)
 
 // prep record layout (bytes, 16-aligned): ent[128] int | u[128] double | st[NBP] int
 __host__ __device__ constexpr int tc_nbp(int G) { return ((G + 1 + 3) / 4) * 4; }
@@ -80,13 +81,15 @@ kan_bwd_tc_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ 
   constexpr int PER = kTcBC / 32;
   int cells[PER];
   double us[PER];
+  unsigned clamped = 0;  // bit q: sample q*32+lane lies outside [g_min, hi] (dx mask = 0)
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int s = q * 32 + lane;
     int cell = -1;
     double u = 0.0;
-    bool mask;
+    bool mask = true;
     if (s < nb) kan_locate(xs[s][warp], grid, cell, u, mask);
+    if (!mask) clamped |= 1u << q;
     cells[q] = cell;
     us[q] = u;
     const unsigned m = tc_same_cell_mask(cell);
@@ -121,7 +124,7 @@ kan_bwd_tc_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ 
     __syncwarp();
     if (cell >= 0) {
       const int pos = base + __popc(m & ((1u << lane) - 1u));
-      ent[pos] = (cell << 8) | (q * 32 + lane);
+      ent[pos] = (cell << 8) | (q * 32 + lane) | (((clamped >> q) & 1u) ? kTcClamped : 0);
       uu[pos] = us[q];
       if (lane == __ffs(m) - 1) cur[cell] = base + __popc(m);
     }
@@ -593,16 +596,9 @@ int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, in
   return UKAN_OK;
 }
 
-int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
-                   void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
-                   const TcPlan& p, cudaStream_t st, bool prepared) {
-  if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
-  unsigned char* recs = reinterpret_cast<unsigned char*>(workspace);
-  double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
-  if (!prepared) {
-    const int rc = kan_bwd_tc_prep(x, workspace, ws_bytes, B, d_in, G, grid, p, st);
-    if (rc) return rc;
-  }
+static int tc_sweep_dispatch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                             unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
+                             cudaStream_t st) {
   if (p.split && p.rb == 8 && p.wpf == 4) return tc2_launch<8, 8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
@@ -617,6 +613,371 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
   if (p.rb == 8) return tc_launch<8, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 16) return tc_launch<16, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   return UKAN_E_ARG;
+}
+
+int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                   void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
+                   const TcPlan& p, cudaStream_t st, bool prepared) {
+  if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
+  unsigned char* recs = reinterpret_cast<unsigned char*>(workspace);
+  double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
+  if (!prepared) {
+    const int rc = kan_bwd_tc_prep(x, workspace, ws_bytes, B, d_in, G, grid, p, st);
+    if (rc) return rc;
+  }
+  return tc_sweep_dispatch(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+}
+
+// ---------------------------------------------------------------------------------------
+// dx on the FP64 tensor cores (wide layers, k = 3, no base branch), from the same sorted records
+// (replaces the per-(sample, feature) warp dot products of spline_dx_kernel, which are bound by
+// the fp32 -> fp64 conversions of every operand):
+//   Q[b, r]  = sum_o g[b, o] * C'[i, r, o]          C' = scale * C, exact in fp64
+//   dx[b, i] = mask * inv_dg * sum_j w'_j(u_b) * Q[b, cell_b + j]       (layers.py:44-46, 84-88,
+//                                                                        tensor.py:330 clamp mask)
+// Task = up to 8 consecutive cell-sorted samples of one feature whose cells lie in [c0, c0+4]:
+// their windows fit rows c0..c0+7, so one m8n8k4 DMMA per 4 outputs computes
+//   D[8 samples x 8 rows] += A[8 samples x 4 outputs] (g) * B[4 outputs x 8 rows] (C'),
+// accumulated over ALL outputs in registers (half of D is outside each sample's window: the
+// banded product's 50% ceiling).  CTA = 4 features x one 256-sample chunk,
+// 16 warps, <= 12 tasks per warp; output tiles of 16: g (fp32, cp.async) and C' (fp64, register
+// prefetch, widened and scaled once per CTA) double-buffered in shared memory, one barrier per
+// tile.  The grid is walked in bands of `band` chunks x all feature groups so a wave shares the
+// band's g rows and a few features' C' through L2.  Deterministic: fixed task order, fixed DMMA
+// order over the outputs, fixed 4-lane reduction.
+// ---------------------------------------------------------------------------------------
+constexpr int kDxF = 4;            // features per CTA
+constexpr int kDxW = 16;           // warps per CTA
+constexpr int kDxOT = 16;          // outputs per staged tile
+constexpr int kDxGS = kDxOT;       // fp32 g row stride (floats, 64 B): a row's bank half = sample & 1
+constexpr int kDxCS = kDxOT + 2;   // fp64 C' row stride (doubles, 144 B): adjacent rows on disjoint banks
+constexpr int kDxMaxT = 12;        // tasks per warp: 4 * (256/8 + G/5 + 1) / 16 <= 12 for G <= 64
+constexpr int kDxTPF = 48;         // task slots per feature (>= 256/8 + 64/5 + 1)
+
+__host__ __device__ constexpr int dx_rr(int G) { return G + 8; }  // C' tile rows: c0 + 7 <= G + 6
+
+struct DxSmem {  // byte offsets of the dynamic shared-memory regions
+  size_t rec, task, g, c, dxs, total;
+};
+__host__ __device__ inline DxSmem dx_smem_layout(int G) {
+  DxSmem L;
+  L.rec = 0;
+  L.task = L.rec + (size_t)kDxF * tc_rec_bytes(G);
+  L.g = L.task + sizeof(int4) * kDxF * kDxTPF + 16;
+  L.c = L.g + sizeof(float) * 2 * (kTcBC + 1) * kDxGS;
+  L.c = (L.c + 15) / 16 * 16;
+  L.dxs = L.c + sizeof(double) * 2 * kDxF * dx_rr(G) * kDxCS;
+  L.total = L.dxs + sizeof(float) * kTcBC * kDxF;
+  return L;
+}
+
+// Position (within a task's sorted run [p0, p1)) whose sample feeds A-row `grp`, or -1 for a
+// padding row.  Samples with even and odd g-tile rows are interleaved so the two rows read by one
+// quarter-warp of the LDS.128 A load sit in different bank halves whenever the run allows it.
+__device__ __forceinline__ int dx_lane_pos(const int* ent, int p0, int p1, int grp) {
+  const int n = p1 - p0;
+  unsigned em = 0, om = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < n) {
+      if (ent[p0 + q] & 1) om |= 1u << q;
+      else em |= 1u << q;
+    }
+  if (grp >= n) return -1;
+  const int ne = __popc(em), no = __popc(om), m = min(ne, no);
+  unsigned mask;
+  int idx;
+  if (grp < 2 * m) {
+    mask = (grp & 1) ? om : em;
+    idx = grp >> 1;
+  } else {
+    mask = ne > no ? em : om;
+    idx = grp - m;
+  }
+  return (int)__fns(mask, 0, idx + 1);
+}
+
+// One staged output tile for NT tasks: per task one LDS.128 of A (4 fp32 g values of this lane's
+// sample) and two LDS.128 of B (4 fp64 C' values of row c0 + grp), then 4 DMMAs.  The k slot of
+// lane kq in DMMA kk is output 4*kq + kk (any fixed k order is valid: A and B use the same one).
+template <int NT>
+__device__ __forceinline__ void dx_tile(const float* __restrict__ gb, const double* __restrict__ cb,
+                                        const uint32_t (&toff)[kDxMaxT], double (&acc)[kDxMaxT][2]) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {  // straight-line: ptxas hoists the loads of later tasks as registers allow
+    const float4 a = *reinterpret_cast<const float4*>(gb + (toff[t] & 0xffffu));
+    const double* cp = cb + (toff[t] >> 16);
+    const double2 b0 = *reinterpret_cast<const double2*>(cp);
+    const double2 b1 = *reinterpret_cast<const double2*>(cp + 2);
+    tc_dmma(acc[t][0], acc[t][1], (double)a.x, b0.x);
+    tc_dmma(acc[t][0], acc[t][1], (double)a.y, b0.y);
+    tc_dmma(acc[t][0], acc[t][1], (double)a.z, b1.x);
+    tc_dmma(acc[t][0], acc[t][1], (double)a.w, b1.y);
+  }
+}
+
+__global__ void __launch_bounds__(kDxW * 32, 1)
+kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C, const float* __restrict__ scale,
+                 const float* __restrict__ gy, float* __restrict__ dx, int B, int d_in, int d_out, int G, int nch,
+                 int n_fg, int band, int ld, double inv_dg, Basis<4> bas) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double Msh[16];
+  __shared__ int cnt_s[kDxF];
+  const DxSmem L = dx_smem_layout(G);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  const int R = G + 3, RR = dx_rr(G);
+  const size_t rb = tc_rec_bytes(G);
+  // banded walk: band b covers chunks [b*band, ...) x all feature groups, feature group major
+  const int64_t lin = blockIdx.x;
+  const int64_t per_band = (int64_t)band * n_fg;
+  const int bnd = (int)(lin / per_band);
+  const int rem = (int)(lin % per_band);
+  const int cb = min(band, nch - bnd * band);
+  const int fg = rem / cb, n = bnd * band + rem % cb;
+  const int i0 = fg * kDxF;
+  const int b0 = n * kTcBC;
+  const int nb = min(kTcBC, B - b0);
+  unsigned char* rec_s = smem_raw + L.rec;
+  int4* task_s = reinterpret_cast<int4*>(smem_raw + L.task);
+  float* g_s = reinterpret_cast<float*>(smem_raw + L.g);
+  double* c_s = reinterpret_cast<double*>(smem_raw + L.c);
+  float* dx_s = reinterpret_cast<float*>(smem_raw + L.dxs);
+  const int GSZ = (kTcBC + 1) * kDxGS, CSZ = kDxF * RR * kDxCS;
+  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  // records of the 4 features (16-byte granules)
+  {
+    const int q = (int)(rb / 16);
+    for (int t = threadIdx.x; t < kDxF * q; t += blockDim.x) {
+      const int f = t / q, c = t % q;
+      const bool ok = i0 + f < d_in;
+      const unsigned char* src = ok ? recs + ((size_t)(i0 + f) * nch + n) * rb + (size_t)c * 16 : recs;
+      tc_cp16(rec_s + (size_t)f * rb + (size_t)c * 16, src, ok ? 16 : 0);
+    }
+  }
+  // zero row 256 of both g buffers (the A operand of padding lanes) and the C' pad rows
+  for (int t = threadIdx.x; t < 2 * kDxGS; t += blockDim.x) g_s[(t / kDxGS) * GSZ + kTcBC * kDxGS + t % kDxGS] = 0.f;
+  const int nq = kDxOT / 4;
+  auto stage_g = [&](int o0, int buf) {
+    float* gd = g_s + buf * GSZ;
+    for (int t = threadIdx.x; t < kTcBC * nq; t += blockDim.x) {
+      const int sm = t / nq, j = (t % nq) * 4;
+      const bool ok = sm < nb && o0 + j < d_out;
+      tc_cp16(gd + sm * kDxGS + j, ok ? gy + (size_t)(b0 + sm) * d_out + o0 + j : gy, ok ? 16 : 0);
+    }
+  };
+  constexpr int CQ = (kDxF * (64 + 8) * (kDxOT / 4) + kDxW * 32 - 1) / (kDxW * 32);  // float4 per thread (G <= 64)
+  float4 cr[CQ];
+  auto load_c = [&](int o0) {
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) {
+      const int t = threadIdx.x + q * kDxW * 32;
+      const int j = (t % nq) * 4, fr = t / nq, r = fr % RR, f = fr / RR;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < kDxF && r < R && i0 + f < d_in && o0 + j < d_out)
+        v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)(i0 + f) * R + r) * d_out + o0 + j));
+      cr[q] = v;
+    }
+  };
+  auto store_c = [&](int o0, int buf) {
+    double* cd = c_s + buf * CSZ;
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) {
+      const int t = threadIdx.x + q * kDxW * 32;
+      const int j = (t % nq) * 4, fr = t / nq, r = fr % RR, f = fr / RR;
+      if (f >= kDxF) continue;
+      float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i0 + f < d_in && o0 + j < d_out) sc = __ldg(reinterpret_cast<const float4*>(scale + (size_t)(i0 + f) * d_out + o0 + j));
+      double* d = cd + ((size_t)f * RR + r) * kDxCS + j;  // C' = scale * C: exact in fp64
+      *reinterpret_cast<double2*>(d) = make_double2((double)cr[q].x * (double)sc.x, (double)cr[q].y * (double)sc.y);
+      *reinterpret_cast<double2*>(d + 2) = make_double2((double)cr[q].z * (double)sc.z, (double)cr[q].w * (double)sc.w);
+    }
+  };
+  const int n_ot = (d_out + kDxOT - 1) / kDxOT;
+  stage_g(0, 0);
+  asm volatile("cp.async.commit_group;\n" ::);
+  load_c(0);
+  store_c(0, 0);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // tasks: greedy runs of <= 8 sorted samples with cells in [c0, c0 + 4] (one thread per feature)
+  if (threadIdx.x < kDxF) {
+    const int f = threadIdx.x;
+    int cnt = 0;
+    if (i0 + f < d_in) {
+      const int* ent = reinterpret_cast<const int*>(rec_s + (size_t)f * rb);
+      int p = 0;
+      while (p < nb) {
+        const int c0 = (ent[p] >> 8) & 127;
+        int q = p + 1;
+        while (q < nb && q - p < 8 && ((ent[q] >> 8) & 127) <= c0 + 4) ++q;
+        task_s[f * kDxTPF + cnt] = make_int4(f, c0, p, q);
+        ++cnt;
+        p = q;
+      }
+    }
+    cnt_s[f] = cnt;
+  }
+  __syncthreads();
+  int T = 0, base_f[kDxF];
+#pragma unroll
+  for (int f = 0; f < kDxF; ++f) {
+    base_f[f] = T;
+    T += cnt_s[f];
+  }
+  const int per = (T + kDxW - 1) / kDxW;
+  const int t_lo = min(T, warp * per), nt = min(per, T - t_lo);
+  // per task: packed smem offsets (A: g row of this lane's sample, B: C' row c0 + grp)
+  auto task_at = [&](int gt) {  // global task index -> its record (feature-major order)
+    int f = 0;
+#pragma unroll
+    for (int ff = 1; ff < kDxF; ++ff)
+      if (gt >= base_f[ff]) f = ff;
+    return task_s[f * kDxTPF + gt - base_f[f]];
+  };
+  uint32_t toff[kDxMaxT];
+#pragma unroll
+  for (int t = 0; t < kDxMaxT; ++t) {
+    toff[t] = 0;
+    if (t < nt) {
+      const int4 ti = task_at(t_lo + t);
+      const int f = ti.x;
+      const int* ent = reinterpret_cast<const int*>(rec_s + (size_t)f * rb);
+      const int q = dx_lane_pos(ent, ti.z, ti.w, grp);
+      const int sm = q >= 0 ? (ent[ti.z + q] & 255) : kTcBC;  // padding lanes read the zero row
+      toff[t] = (uint32_t)(sm * kDxGS + 4 * kq) | ((uint32_t)((f * RR + ti.y + grp) * kDxCS + 4 * kq) << 16);
+    }
+  }
+  double acc[kDxMaxT][2];
+#pragma unroll
+  for (int t = 0; t < kDxMaxT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  for (int ot = 0; ot < n_ot; ++ot) {
+    const int buf = ot & 1;
+    const bool more = ot + 1 < n_ot;
+    if (more) {
+      stage_g((ot + 1) * kDxOT, buf ^ 1);
+      asm volatile("cp.async.commit_group;\n" ::);
+      load_c((ot + 1) * kDxOT);
+    }
+    const float* gb = g_s + buf * GSZ;
+    const double* cbuf = c_s + buf * CSZ;
+    switch (nt) {  // warp-uniform: a fully unrolled, predicate-free body per task count
+      case 1: dx_tile<1>(gb, cbuf, toff, acc); break;
+      case 2: dx_tile<2>(gb, cbuf, toff, acc); break;
+      case 3: dx_tile<3>(gb, cbuf, toff, acc); break;
+      case 4: dx_tile<4>(gb, cbuf, toff, acc); break;
+      case 5: dx_tile<5>(gb, cbuf, toff, acc); break;
+      case 6: dx_tile<6>(gb, cbuf, toff, acc); break;
+      case 7: dx_tile<7>(gb, cbuf, toff, acc); break;
+      case 8: dx_tile<8>(gb, cbuf, toff, acc); break;
+      case 9: dx_tile<9>(gb, cbuf, toff, acc); break;
+      case 10: dx_tile<10>(gb, cbuf, toff, acc); break;
+      case 11: dx_tile<11>(gb, cbuf, toff, acc); break;
+      case 12: dx_tile<12>(gb, cbuf, toff, acc); break;
+      default: break;
+    }
+    if (more) {
+      store_c((ot + 1) * kDxOT, buf ^ 1);
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+  }
+  // epilogue: lane (grp, kq) holds Q[sample grp][rows c0 + 2kq, c0 + 2kq + 1]
+#pragma unroll
+  for (int t = 0; t < kDxMaxT; ++t) {
+    if (t < nt) {
+      const int4 ti = task_at(t_lo + t);
+      const int f = ti.x;
+      const int q = dx_lane_pos(reinterpret_cast<const int*>(rec_s + (size_t)f * rb), ti.z, ti.w, grp);
+      const int pos = ti.z + max(q, 0);
+      const bool vld = q >= 0;
+      const unsigned char* rec = rec_s + (size_t)f * rb;
+      const int e = vld ? reinterpret_cast<const int*>(rec)[pos] : 0;
+      const double u = vld ? reinterpret_cast<const double*>(rec + kTcBC * 4)[pos] : 0.0;
+      const int cell = (e >> 8) & 127;
+      double part = 0.0;
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = ti.y + 2 * kq + v - cell;
+        if (vld && j >= 0 && j < 4) {  // w'_j(u) = M1j + 2 u M2j + 3 u^2 M3j (layers.py:29-37, d = 1)
+          const double wp = fma(fma(3.0 * Msh[12 + j], u, 2.0 * Msh[8 + j]), u, Msh[4 + j]);
+          part = fma(wp, acc[t][v], part);
+        }
+      }
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (vld && kq == 0) dx_s[(e & 255) * kDxF + f] = (e & kTcClamped) ? 0.f : (float)(part * inv_dg);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nb * kDxF; t += blockDim.x) {
+    const int sm = t / kDxF, f = t % kDxF;
+    if (i0 + f < d_in) dx[(size_t)(b0 + sm) * ld + i0 + f] = dx_s[t];
+  }
+}
+
+bool kan_dx_tc_applicable(const TcPlan& p, const float* C, const float* gy, int d_out, int G) {
+  static const bool off = getenv("UKAN_DX") && getenv("UKAN_DX")[0] == 's';  // A/B: the SIMT dx kernel
+  return !off && p.ok && G <= 64 && d_out >= 64 && d_out % 4 == 0 && ((uintptr_t)C % 16) == 0 &&
+         ((uintptr_t)gy % 16) == 0;
+}
+
+// dx from the records kan_bwd_tc_prep left in `recs` (features [0, d_in) of the pointers given;
+// dx rows have stride ld).
+static int dx_tc_launch(const float* C, const float* scale, const float* gy, float* dx, const unsigned char* recs,
+                        int B, int d_in, int d_out, int G, int nch, int ld, const KanGrid& grid, cudaStream_t st) {
+  const DxSmem L = dx_smem_layout(G);
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kan_dx_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  const int n_fg = (d_in + kDxF - 1) / kDxF;
+  static const int band_env = getenv("UKAN_DX_BAND") ? atoi(getenv("UKAN_DX_BAND")) : 16;
+  const int band = std::max(1, std::min(band_env, nch));
+  const int64_t nblk = (int64_t)nch * n_fg;
+  kan_dx_tc_kernel<<<(unsigned)nblk, kDxW * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg,
+                                                                band, ld, grid.inv_dg, make_basis<4>(3));
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
+int kan_dx_tc_run(const float* C, const float* scale, const float* gy, float* dx, void* workspace, int B, int d_in,
+                  int d_out, int G, const KanGrid& grid, const TcPlan& p, cudaStream_t st) {
+  return dx_tc_launch(C, scale, gy, dx, reinterpret_cast<const unsigned char*>(workspace), B, d_in, d_out, G, p.nch,
+                      d_in, grid, st);
+}
+
+// One part of the backward over features [i_lo, i_hi), from records prepared for the WHOLE layer
+// (kan_bwd_tc_prep on the same workspace): what & 1 = table gradient (dC, dscale of those
+// features), what & 2 = dx of those features.  Lets a data-parallel caller all-reduce finished
+// feature slices of dC while later slices are still being computed.
+int kan_bwd_tc_part(const float* C, const float* scale, const float* gy, float* dx, float* dC, float* dscale,
+                    void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
+                    int64_t i_lo, int64_t i_hi, int what, cudaStream_t st) {
+  const TcPlan full = kan_bwd_tc_plan(B, d_in, d_out, G, 3, false);
+  if (!full.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(full)) return UKAN_E_WORKSPACE;
+  if (i_lo < 0 || i_hi > d_in || i_lo >= i_hi) return UKAN_E_ARG;
+  const int n = (int)(i_hi - i_lo), R = G + 3;
+  unsigned char* base = reinterpret_cast<unsigned char*>(workspace);
+  const unsigned char* recs = base + (size_t)i_lo * full.nch * tc_rec_bytes(G);
+  if (what & 1) {
+    if (!dC || !dscale) return UKAN_E_ARG;
+    TcPlan p = kan_bwd_tc_plan(B, n, d_out, G, 3, false);
+    double* part = reinterpret_cast<double*>(base + ((full.rec_bytes + 255) / 256) * 256);
+    if (p.S > 1 && p.part_bytes > full.part_bytes) {  // the slice's split-K partials must fit the workspace
+      p.S = 1;
+      p.cps = p.nch;
+      p.part_bytes = 0;
+    }
+    const int rc = tc_sweep_dispatch(C + (size_t)i_lo * R * d_out, scale + (size_t)i_lo * d_out, gy,
+                                     dC + (size_t)i_lo * R * d_out, dscale + (size_t)i_lo * d_out,
+                                     const_cast<unsigned char*>(recs), part, B, n, d_out, G, p, st);
+    if (rc) return rc;
+  }
+  if (what & 2) {
+    if (!dx) return UKAN_E_ARG;
+    if (!kan_dx_tc_applicable(full, C, gy, d_out, G)) return UKAN_E_ARG;
+    return dx_tc_launch(C + (size_t)i_lo * R * d_out, scale + (size_t)i_lo * d_out, gy, dx + i_lo, recs, B, n, d_out,
+                        G, full.nch, d_in, grid, st);
+  }
+  return UKAN_OK;
 }
 
 }  // namespace ukan

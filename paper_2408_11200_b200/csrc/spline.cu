@@ -511,6 +511,12 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
                    const TcPlan& p, cudaStream_t st, bool prepared);
 int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, int d_in, int G, const KanGrid& grid,
                     const TcPlan& p, cudaStream_t st);
+bool kan_dx_tc_applicable(const TcPlan& p, const float* C, const float* gy, int d_out, int G);
+int kan_bwd_tc_part(const float* C, const float* scale, const float* gy, float* dx, float* dC, float* dscale,
+                    void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int G, const KanGrid& grid,
+                    int64_t i_lo, int64_t i_hi, int what, cudaStream_t st);
+int kan_dx_tc_run(const float* C, const float* scale, const float* gy, float* dx, void* workspace, int B, int d_in,
+                  int d_out, int G, const KanGrid& grid, const TcPlan& p, cudaStream_t st);
 bool kan_bwd_dmma_plan(int64_t B, int64_t d_in, int64_t d_out, int R, int K, bool has_base, int sms, RegPlan& p);
 int kan_bwd_dmma_dispatch(const float* x, const float* C, const float* scale, const float* gy, float* dC,
                           float* dscale, double* ws, int B, int d_in, int d_out, int R, const KanGrid& grid,
@@ -819,6 +825,9 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
       if (ss) return UKAN_OK;
       if (dx) {
         if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+        // wide layers: dx on the FP64 tensor cores from the same sorted records (kan_bwd_tc.cu)
+        if (kan_dx_tc_applicable(tp, coeffs, gy, d_out, rm.R - K + 1))
+          return kan_dx_tc_run(coeffs, scale, gy, dx, workspace, B, d_in, d_out, rm.R - K + 1, rm.grid, tp, st);
         const Basis<K> bas = make_basis<K>(K - 1);
         const int64_t pairs = (int64_t)B * d_in;
         spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
@@ -897,6 +906,26 @@ extern "C" int ukan_kan_backward_ws2(const float* x, const float* coeffs, const 
   cudaStream_t st = (cudaStream_t)stream;
   UKAN_DISPATCH_K(k, return kan_backward_impl<K>(x, coeffs, scale, base_weight, gy, dx, dcoeffs, dscale, dbase_weight, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out, rm, st, (flags & 1) != 0););
   return UKAN_OK;
+}
+
+extern "C" int ukan_kan_backward_part_supported(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k) {
+  if (check_kan_args(B, d_in, d_out, G, k, -1.0, 1.0) || B < 1) return 0;
+  if (kan_bwd_selector()[0] != 't') return 0;
+  const TcPlan p = kan_bwd_tc_plan(B, d_in, d_out, G, k, false);
+  return (p.ok && d_out >= 64 && d_out % 4 == 0) ? 1 : 0;
+}
+
+extern "C" int ukan_kan_backward_part(const float* coeffs, const float* scale, const float* gy, float* dx,
+                                      float* dcoeffs, float* dscale, int64_t B, int64_t d_in, int64_t d_out,
+                                      int64_t G, int k, double g_min, double g_max, void* workspace,
+                                      int64_t workspace_bytes, int64_t i_lo, int64_t i_hi, int what, void* stream) {
+  int rc = check_kan_args(B, d_in, d_out, G, k, g_min, g_max);
+  if (rc) return rc;
+  if (!ukan_kan_backward_part_supported(B, d_in, d_out, G, k)) return UKAN_E_ARG;
+  if (!coeffs || !scale || !gy || (what & ~3) || what == 0) return UKAN_E_ARG;
+  const KanGrid grid = make_kan_grid(g_min, g_max, G);
+  return kan_bwd_tc_part(coeffs, scale, gy, dx, dcoeffs, dscale, workspace, workspace_bytes, (int)B, (int)d_in,
+                         (int)d_out, (int)G, grid, i_lo, i_hi, what, (cudaStream_t)stream);
 }
 
 extern "C" int ukan_kan_backward_ws(const float* x, const float* coeffs, const float* scale,

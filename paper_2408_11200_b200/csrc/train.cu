@@ -12,18 +12,24 @@ namespace ukan {
 // per-row CE loss (fp64) and gradient
 __global__ void xent_rows_kernel(const float* __restrict__ logits, const int64_t* __restrict__ labels,
                                  double* __restrict__ row_loss, float* __restrict__ dlogits,
-                                 int64_t n, int c, double gscale_over_n) {
+                                 int64_t n, int c, double gscale_over_n, int32_t* __restrict__ err) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const float* z = logits + (size_t)r * c;
+  const int64_t lab = labels[r];
+  float* dz = dlogits + (size_t)r * c;
+  if (lab < 0 || lab >= c) {  // the reference indexes logp[rows, labels] and raises IndexError
+    row_loss[r] = NAN;        // (tensor.py:388-392): flag it (read_loss raises), never read OOB
+    for (int j = 0; j < c; ++j) dz[j] = 0.f;
+    if (err) atomicOr(err, 2);
+    return;
+  }
   double mx = -INFINITY;
   for (int j = 0; j < c; ++j) mx = fmax(mx, (double)z[j]);
   double se = 0.0;
   for (int j = 0; j < c; ++j) se += exp((double)z[j] - mx);
   const double lse = log(se);
-  const int64_t lab = labels[r];
   row_loss[r] = -(((double)z[lab] - mx) - lse);
-  float* dz = dlogits + (size_t)r * c;
   for (int j = 0; j < c; ++j) {
     double p = exp(((double)z[j] - mx) - lse);
     if (j == lab) p -= 1.0;
@@ -75,7 +81,9 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
 
 // Graph-replayable Adam: the step counter, learning rate and bias corrections live on the device
 // (a captured CUDA graph replays the same launch parameters every step).
-__global__ void adam_count_kernel(int64_t* __restrict__ t, double b1, double b2, double* __restrict__ bc) {
+__global__ void adam_count_kernel(int64_t* __restrict__ t, double b1, double b2, double* __restrict__ bc,
+                                  const double* __restrict__ guard) {
+  if (guard && !isfinite(*guard)) return;  // skipped step: the reference raises before state.t += 1
   const int64_t tt = t[0] + 1;
   t[0] = tt;
   bc[0] = 1.0 - pow(b1, (double)tt);  // optim.py:38-39
@@ -120,12 +128,12 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 
 extern "C" int ukan_softmax_xent(const float* logits, const int64_t* labels, double* loss,
                                  float* dlogits, int64_t n, int64_t c, int64_t n_global,
-                                 double grad_scale, void* stream) {
+                                 double grad_scale, int32_t* err_flag, void* stream) {
   if (n < 1 || c < 1 || n_global < 1 || !logits || !labels || !loss || !dlogits) return UKAN_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   double* rows = reinterpret_cast<double*>(loss) + 1;  // caller provides loss[1 + n] doubles
   xent_rows_kernel<<<nblk(n, 256), 256, 0, st>>>(logits, labels, rows, dlogits, n, (int)c,
-                                                  grad_scale / (double)n_global);
+                                                  grad_scale / (double)n_global, err_flag);
   UKAN_LAUNCH_CHECK();
   sum_f64_kernel<<<1, 1024, 0, st>>>(rows, n, 1.0 / (double)n_global, loss);
   UKAN_LAUNCH_CHECK();
@@ -162,7 +170,7 @@ extern "C" int ukan_adam_step_dev(float* p, const float* g, float* m, float* v, 
                                   double* bc, const double* guard, void* stream) {
   if (n < 0 || !p || !g || !m || !v || !lr || !t || !bc) return UKAN_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  adam_count_kernel<<<1, 1, 0, st>>>(t, beta1, beta2, bc);
+  adam_count_kernel<<<1, 1, 0, st>>>(t, beta1, beta2, bc, guard);
   UKAN_LAUNCH_CHECK();
   if (n == 0) return UKAN_OK;
   adam_dev_kernel<<<nblk(n, 256), 256, 0, st>>>(p, g, m, v, n, lr, beta1, beta2, eps, weight_decay, bc, guard);

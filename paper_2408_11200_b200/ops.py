@@ -67,6 +67,7 @@ class KanSplineFn(torch.autograd.Function):
     def forward(ctx, x, coeffs, scale, base_weight, G: int, k: int, g_min: float, g_max: float):
         lib = _lib.load()
         _lib.require_cuda(x, coeffs, scale, base_weight)
+        _lib.require_params(x.device, coeffs, scale, base_weight)
         x = _f32(x)
         B, d_in = x.shape
         d_out = coeffs.shape[2]
@@ -197,63 +198,92 @@ def ukan_build_keys(x: torch.Tensor, k: int, delta_g: float, max_keys: int | Non
     return UkanKeys(key_f[:n], key_g[:n], seg_start, base_row, n, int(max_rows.value))
 
 
+def cg_forward_raw(key_f, key_g, emb, w1, b1, w2, b2, d_pe: int, table_out=None):
+    """_cg_eval (layers.py:232-243) on raw buffers, fp64 between the GEMMs:
+    inp64 = [emb[f] || PE(g)] (fp64 PE), pre64 = inp64 @ W1 + b1 and H64 = silu(pre64) on the FP64
+    tensor cores, H32 = (float)H64, table = H32 @ W2 + b2 on tcgen05 (tf32 pieces, fp32-exact
+    products).  Returns (table [n_u, K*d_out] fp32, cache for ``cg_backward_raw``)."""
+    lib = _lib.load()
+    n_u = key_f.shape[0]
+    d_femb = emb.shape[1]
+    d_cg_in, d_h = w1.shape
+    n_out = w2.shape[1]
+    dev = emb.device
+    st = stream_ptr()
+    inp = torch.empty((n_u, d_cg_in), device=dev, dtype=torch.float64)
+    pre = torch.empty((n_u, d_h), device=dev, dtype=torch.float64)
+    H64 = torch.empty((n_u, d_h), device=dev, dtype=torch.float64)
+    H32 = torch.empty((n_u, d_h), device=dev, dtype=torch.float32)
+    table = table_out if table_out is not None else torch.empty((n_u, n_out), device=dev, dtype=torch.float32)
+    if n_u > 0:
+        check(lib.ukan_ukan_cg_input(ptr(key_f), ptr(key_g), ptr(emb), ptr(inp), n_u, d_femb, d_pe, st), "cg_input")
+        check(lib.ukan_gemm_f64(0, ptr(inp), _lib.UKAN_F64, ptr(w1), _lib.UKAN_F32, ptr(b1), 1, ptr(pre), ptr(H32),
+                                ptr(H64), None, n_u, d_h, d_cg_in, st), "cg_gemm1")
+        check(lib.ukan_gemm_bias_act(ptr(H32), ptr(w2), ptr(b2), ptr(table), None, n_u, n_out, d_h, 0, st),
+              "cg_gemm2")
+    return table, (inp, pre, H64)
+
+
+def cg_backward_raw(cache, dtable, w1, w2, seg_start, d_femb: int, dw1, db1, dw2, db2, demb):
+    """Tape backward of _cg_eval (matmul / silu / gather_rows / concat_last, tensor.py:189-197,
+    228-233, 257-268, 276-285) given dtable [n_u, K*d_out]: every GEMM on the FP64 tensor cores
+    with fp64 intermediates (dH, dpre, dinp); gradients WRITTEN into dw1, db1, dw2, db2 and (if
+    not None) demb."""
+    lib = _lib.load()
+    inp, pre, H64 = cache
+    n_u, d_cg_in = inp.shape
+    d_h = H64.shape[1]
+    n_out = w2.shape[1]
+    d_in = seg_start.shape[0] - 1
+    dev = inp.device
+    st = stream_ptr()
+    if n_u == 0:
+        for t in (dw1, db1, dw2, db2, demb):
+            if t is not None:
+                t.zero_()
+        return
+    F32, F64 = _lib.UKAN_F32, _lib.UKAN_F64
+    check(lib.ukan_gemm_f64(2, ptr(H64), F64, ptr(dtable), F32, None, 0, None, ptr(dw2), None, ptr(db2), d_h, n_out,
+                            n_u, st), "cg_dW2")
+    dH = torch.empty((n_u, d_h), device=dev, dtype=torch.float64)
+    check(lib.ukan_gemm_f64(1, ptr(dtable), F32, ptr(w2), F32, None, 0, None, None, ptr(dH), None, n_u, d_h, n_out,
+                            st), "cg_dH")
+    dpre = torch.empty_like(dH)
+    check(lib.ukan_silu_backward(ptr(pre), ptr(dH), ptr(dpre), dH.numel(), st), "cg_dsilu")
+    check(lib.ukan_gemm_f64(2, ptr(inp), F64, ptr(dpre), F64, None, 0, None, ptr(dw1), None, ptr(db1), d_cg_in, d_h,
+                            n_u, st), "cg_dW1")
+    if demb is not None:
+        dinp = torch.empty_like(inp)
+        check(lib.ukan_gemm_f64(1, ptr(dpre), F64, ptr(w1), F32, None, 0, None, None, ptr(dinp), None, n_u, d_cg_in,
+                                d_h, st), "cg_dinp")
+        check(lib.ukan_ukan_emb_backward(ptr(seg_start), ptr(dinp), ptr(demb), d_in, d_femb, d_cg_in, st), "cg_demb")
+
+
 class CgMlpFn(torch.autograd.Function):
     """Coefficient generator over unique keys (layers.py:232-243):
     table = silu([emb[f] || PE(g)] @ W1 + b1) @ W2 + b2  ->  [n_u, K*d_out] (slot-major)."""
 
     @staticmethod
     def forward(ctx, emb, w1, b1, w2, b2, key_f, key_g, seg_start, d_pe: int):
-        lib = _lib.load()
         _lib.require_cuda(emb, w1, b1, w2, b2)
-        n_u = key_f.shape[0]
-        d_femb = emb.shape[1]
-        d_cg_in, d_h = w1.shape
-        n_out = w2.shape[1]
-        dev = emb.device
-        inp = torch.empty((n_u, d_cg_in), device=dev, dtype=torch.float32)
-        pre = torch.empty((n_u, d_h), device=dev, dtype=torch.float32)
-        H = torch.empty((n_u, d_h), device=dev, dtype=torch.float32)
-        table = torch.empty((n_u, n_out), device=dev, dtype=torch.float32)
-        st = stream_ptr()
-        check(lib.ukan_ukan_cg_input(ptr(key_f), ptr(key_g), ptr(emb), ptr(inp), n_u, d_femb, d_pe, st),
-              "cg_input")
-        check(lib.ukan_gemm_bias_act(ptr(inp), ptr(w1), ptr(b1), ptr(H), ptr(pre), n_u, d_h, d_cg_in, 1, st),
-              "cg_gemm1")
-        check(lib.ukan_gemm_bias_act(ptr(H), ptr(w2), ptr(b2), ptr(table), None, n_u, n_out, d_h, 0, st),
-              "cg_gemm2")
-        ctx.save_for_backward(inp, pre, H, w1, w2, seg_start)
-        ctx.d_femb = d_femb
+        _lib.require_params(emb.device, emb, w1, b1, w2, b2)
+        table, cache = cg_forward_raw(key_f, key_g, emb, w1, b1, w2, b2, d_pe)
+        ctx.save_for_backward(*cache, w1, w2, seg_start)
+        ctx.d_femb = emb.shape[1]
         return table
 
     @staticmethod
     def backward(ctx, dtable):
-        lib = _lib.load()
-        inp, pre, H, w1, w2, seg_start = ctx.saved_tensors
+        inp, pre, H64, w1, w2, seg_start = ctx.saved_tensors
         dtable = _f32(dtable)
-        n_u, d_cg_in = inp.shape
-        d_h = H.shape[1]
-        n_out = w2.shape[1]
+        dev = inp.device
         d_femb = ctx.d_femb
         d_in = seg_start.shape[0] - 1
-        dev = inp.device
-        st = stream_ptr()
-        dw2 = torch.empty_like(w2)
-        db2 = torch.empty(n_out, device=dev, dtype=torch.float32)
-        check(lib.ukan_gemm_tn(ptr(H), ptr(dtable), ptr(dw2), ptr(db2), d_h, n_out, n_u, st), "cg_dW2")
-        dH = torch.empty((n_u, d_h), device=dev, dtype=torch.float32)
-        check(lib.ukan_gemm_nt(ptr(dtable), ptr(w2), ptr(dH), n_u, d_h, n_out, st), "cg_dH")
-        dpre = torch.empty_like(dH)
-        check(lib.ukan_silu_backward(ptr(pre), ptr(dH), ptr(dpre), dH.numel(), st), "cg_dsilu")
-        dw1 = torch.empty_like(w1)
-        db1 = torch.empty(d_h, device=dev, dtype=torch.float32)
-        check(lib.ukan_gemm_tn(ptr(inp), ptr(dpre), ptr(dw1), ptr(db1), d_cg_in, d_h, n_u, st), "cg_dW1")
-        demb = None
-        if ctx.needs_input_grad[0]:
-            dinp = torch.empty_like(inp)
-            check(lib.ukan_gemm_nt(ptr(dpre), ptr(w1), ptr(dinp), n_u, d_cg_in, d_h, st), "cg_dinp")
-            demb = torch.empty((d_in, d_femb), device=dev, dtype=torch.float32)
-            check(lib.ukan_ukan_emb_backward(ptr(seg_start), ptr(dinp), ptr(demb), d_in, d_femb, d_cg_in, st),
-                  "cg_demb")
+        dw1, dw2 = torch.empty_like(w1), torch.empty_like(w2)
+        db1 = torch.empty(w1.shape[1], device=dev, dtype=torch.float32)
+        db2 = torch.empty(w2.shape[1], device=dev, dtype=torch.float32)
+        demb = torch.empty((d_in, d_femb), device=dev, dtype=torch.float32) if ctx.needs_input_grad[0] else None
+        cg_backward_raw((inp, pre, H64), dtable, w1, w2, seg_start, d_femb, dw1, db1, dw2, db2, demb)
         return demb, dw1, db1, dw2, db2, None, None, None, None
 
 
@@ -264,6 +294,7 @@ class UkanSplineFn(torch.autograd.Function):
     def forward(ctx, x, table, scale, base_row, seg_start, k: int, delta_g: float):
         lib = _lib.load()
         _lib.require_cuda(x, table, scale)
+        _lib.require_params(x.device, table, scale)
         x = _f32(x)
         B, d_in = x.shape
         d_out = scale.shape[1]
@@ -304,6 +335,7 @@ class KanJvpFn(torch.autograd.Function):
     def forward(ctx, x, tx, coeffs, scale, base_weight, G: int, k: int, g_min: float, g_max: float):
         lib = _lib.load()
         _lib.require_cuda(x, tx, coeffs, scale, base_weight)
+        _lib.require_params(x.device, coeffs, scale, base_weight)
         x, tx = _f32(x), _f32(tx)
         B, d_in = x.shape
         d_out = coeffs.shape[2]
@@ -342,6 +374,7 @@ class UkanJvpFn(torch.autograd.Function):
     def forward(ctx, x, tx, table, scale, base_row, seg_start, k: int, delta_g: float):
         lib = _lib.load()
         _lib.require_cuda(x, tx, table, scale)
+        _lib.require_params(x.device, table, scale)
         x, tx = _f32(x), _f32(tx)
         B, d_in = x.shape
         d_out = scale.shape[1]

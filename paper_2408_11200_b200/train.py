@@ -22,7 +22,7 @@ import torch.distributed as dist
 
 from . import _lib
 from ._lib import check, ptr, stream_ptr
-from .errors import ConfigError, DivergedError
+from .errors import ConfigError, DimensionError, DivergedError
 from .layers import KanLayer, Model, UkanLayer
 from . import ops
 
@@ -147,24 +147,12 @@ class SplineTrainer:
             return y, None
         keys = ops.ukan_build_keys(h, layer.k, float(layer.delta_g))
         self.kernel_launches += 5
-        n_u = keys.n_u
-        d_h = layer.cg_w1.shape[1]
-        d_cg = layer.cg_w1.shape[0]
-        n_out = layer.cg_w2.shape[1]
-        inp = torch.empty((n_u, d_cg), device=self.device, dtype=torch.float32)
-        pre = torch.empty((n_u, d_h), device=self.device, dtype=torch.float32)
-        H = torch.empty_like(pre)
-        table = torch.empty((n_u, n_out), device=self.device, dtype=torch.float32)
-        check(self.lib.ukan_ukan_cg_input(ptr(keys.key_f), ptr(keys.key_g), ptr(layer.feature_embedding), ptr(inp),
-                                          n_u, layer.d_femb, layer.d_pe, st), "cg_input")
-        check(self.lib.ukan_gemm_bias_act(ptr(inp), ptr(layer.cg_w1), ptr(layer.cg_b1), ptr(H), ptr(pre), n_u, d_h,
-                                          d_cg, 1, st), "cg_gemm1")
-        check(self.lib.ukan_gemm_bias_act(ptr(H), ptr(layer.cg_w2), ptr(layer.cg_b2), ptr(table), None, n_u, n_out,
-                                          d_h, 0, st), "cg_gemm2")
+        table, cg_cache = ops.cg_forward_raw(keys.key_f, keys.key_g, layer.feature_embedding, layer.cg_w1,
+                                             layer.cg_b1, layer.cg_w2, layer.cg_b2, layer.d_pe)
         check(self.lib.ukan_ukan_forward(ptr(h), ptr(keys.base_row), ptr(table), ptr(layer.scale), ptr(y), B,
                                          layer.d_in, layer.d_out, layer.k, float(layer.delta_g), st), "ukan_forward")
         self.kernel_launches += 4
-        return y, (keys, inp, pre, H, table)
+        return y, (keys, cg_cache, table)
 
     def _prep_first_layer(self, layer, x):
         """The first layer's backward records depend on x only: build them on a side stream while
@@ -213,11 +201,8 @@ class SplineTrainer:
                                                  float(layer.g_max), ptr(ws), nbytes, flags, st), "kan_backward")
             self.kernel_launches += 2 if need_dx else 1
             return dx
-        keys, inp, pre, H, table = cache
+        keys, cg_cache, table = cache
         n_u = keys.n_u
-        d_h = H.shape[1]
-        d_cg = inp.shape[1]
-        n_out = table.shape[1]
         dtable = torch.empty_like(table)
         nbytes = self.lib.ukan_ukan_backward_workspace_size(B, layer.d_in, layer.d_out, n_u, layer.k)
         ws = torch.empty(max(nbytes, 8), device=self.device, dtype=torch.uint8)
@@ -225,30 +210,66 @@ class SplineTrainer:
                                           ptr(layer.scale), ptr(gy), ptr(dx), ptr(dtable), ptr(gv[pre_ + "scale"]),
                                           B, layer.d_in, layer.d_out, n_u, layer.k, float(layer.delta_g), ptr(ws),
                                           nbytes, st), "ukan_backward")
-        check(self.lib.ukan_gemm_tn(ptr(H), ptr(dtable), ptr(gv[pre_ + "cg_w2"]), ptr(gv[pre_ + "cg_b2"]), d_h, n_out,
-                                    n_u, st), "cg_dW2")
-        dH = torch.empty_like(H)
-        check(self.lib.ukan_gemm_nt(ptr(dtable), ptr(layer.cg_w2), ptr(dH), n_u, d_h, n_out, st), "cg_dH")
-        dpre = torch.empty_like(H)
-        check(self.lib.ukan_silu_backward(ptr(pre), ptr(dH), ptr(dpre), dH.numel(), st), "cg_dsilu")
-        check(self.lib.ukan_gemm_tn(ptr(inp), ptr(dpre), ptr(gv[pre_ + "cg_w1"]), ptr(gv[pre_ + "cg_b1"]), d_cg, d_h,
-                                    n_u, st), "cg_dW1")
-        dinp = torch.empty_like(inp)
-        check(self.lib.ukan_gemm_nt(ptr(dpre), ptr(layer.cg_w1), ptr(dinp), n_u, d_cg, d_h, st), "cg_dinp")
-        check(self.lib.ukan_ukan_emb_backward(ptr(keys.seg_start), ptr(dinp), ptr(gv[pre_ + "feature_embedding"]),
-                                              layer.d_in, layer.d_femb, d_cg, st), "cg_demb")
+        ops.cg_backward_raw(cg_cache, dtable, layer.cg_w1, layer.cg_w2, keys.seg_start, layer.d_femb,
+                            gv[pre_ + "cg_w1"], gv[pre_ + "cg_b1"], gv[pre_ + "cg_w2"], gv[pre_ + "cg_b2"],
+                            gv[pre_ + "feature_embedding"])
         self.kernel_launches += 10 + (1 if need_dx else 0)
         return dx
+
+    # -- input checks (the reference's DimensionError / IndexError, tensor.py:368-400) ---------
+    def _checked_inputs(self, x: torch.Tensor, target: torch.Tensor):
+        """fp32 contiguous x on this device with d_in columns; int64 labels (CE) or an fp32 target
+        with one value per output (MSE).  Label RANGE is checked on the device (no sync): the loss
+        kernel flags it and ``read_loss`` raises IndexError."""
+        layers = self.model.layers
+        if not (isinstance(x, torch.Tensor) and isinstance(target, torch.Tensor)):
+            raise TypeError("x and target must be torch tensors on the trainer's device")
+        if x.device != self.device or target.device != self.device:
+            raise ConfigError(f"x / target must live on {self.device}")
+        if x.dim() != 2 or x.shape[1] != layers[0].d_in:
+            raise DimensionError(f"x must be [B, {layers[0].d_in}], got {tuple(x.shape)}")
+        if x.dtype != torch.float32 or not x.is_contiguous():
+            x = x.float().contiguous()
+        B = x.shape[0]
+        d_last = layers[-1].d_out
+        if self.loss_kind == "softmax_cross_entropy":
+            if target.dim() != 1 or target.shape[0] != B:
+                raise DimensionError(f"labels must be [{B}], got {tuple(target.shape)}")
+            if target.dtype.is_floating_point or target.dtype == torch.bool:
+                raise DimensionError(f"labels must be integers, got {target.dtype}")
+            if target.dtype != torch.int64 or not target.is_contiguous():
+                target = target.long().contiguous()
+        else:
+            if target.numel() != B * d_last:
+                raise DimensionError(f"target must hold {B}x{d_last} values, got {tuple(target.shape)}")
+            if target.dtype != torch.float32 or not target.is_contiguous():
+                target = target.float().contiguous()
+        return x, target
+
+    def _global_batch(self, B: int) -> int:
+        """Global batch = sum of the shard sizes (uneven shards allowed): all-reduced once per
+        local shape and cached, so every rank normalises by the same number."""
+        if not self.sync.enabled:
+            return B
+        cache = self.__dict__.setdefault("_n_global_cache", {})
+        if B not in cache:
+            t = torch.tensor([B], dtype=torch.int64, device=self.device if dist.get_backend(self.sync.group) == "nccl"
+                             else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.sync.group)
+            cache[B] = int(t.item())
+        return cache[B]
 
     # -- the step --------------------------------------------------------------------------
     def step(self, x: torch.Tensor, target: torch.Tensor, n_global: int | None = None, lr: float | None = None):
         """One DP training step on this rank's shard (x, target already on the device).
-        Returns the device fp64 global loss (read it with ``read_loss``)."""
+        Returns the device fp64 global loss (read it with ``read_loss``).  ``n_global`` defaults
+        to the sum of every rank's shard size."""
+        x, target = self._checked_inputs(x, target)
         st = stream_ptr()
         layers = self.model.layers
         B = x.shape[0]
         if n_global is None:
-            n_global = B * self.sync.world
+            n_global = self._global_batch(B)
         if getattr(self, "_err", None) is None:
             self._err = torch.zeros(1, device=self.device, dtype=torch.int32)
         else:  # reset the NaN flag with our fill kernel (0.0f has the all-zero bit pattern)
@@ -270,7 +291,7 @@ class SplineTrainer:
         gy = torch.empty_like(out)
         if self.loss_kind == "softmax_cross_entropy":
             check(self.lib.ukan_softmax_xent(ptr(out), ptr(target), ptr(self._loss_buf), ptr(gy), B, out.shape[1],
-                                             n_global, 1.0, st), "softmax_xent")
+                                             n_global, 1.0, ptr(self._err), st), "softmax_xent")
         else:
             n_el = out.numel()
             check(self.lib.ukan_mse(ptr(out), ptr(target), ptr(self._loss_buf), ptr(gy), n_el,
@@ -283,11 +304,13 @@ class SplineTrainer:
             lo, hi = self.flat.layer_slice(i, self.model)
             self.sync.allreduce_async(self.flat.grad[lo:hi])
         self.sync.wait()
-        self.t += 1
+        self.t += 1  # undone by read_loss if this step's loss diverged (the update is skipped)
         lr = self.lr if lr is None else lr
         n = self.flat.data.numel()
         if self.optimizer == "adam" and self._dev_state is not None:  # graph-replayable form
             t_dev, lr_dev, bc = self._dev_state
+            if not torch.cuda.is_current_stream_capturing():
+                lr_dev.fill_(lr)  # eager step after capture(): honour lr / self.lr
             check(self.lib.ukan_adam_step_dev(ptr(self.flat.data), ptr(self.flat.grad), ptr(self.m), ptr(self.v), n,
                                               ptr(lr_dev), self.beta1, self.beta2, self.eps, self.wd, ptr(t_dev),
                                               ptr(bc), ptr(loss), st), "adam_dev")
@@ -298,6 +321,7 @@ class SplineTrainer:
         else:
             check(self.lib.ukan_sgd_step(ptr(self.flat.data), ptr(self.flat.grad), n, lr, ptr(loss), st), "sgd")
         self.kernel_launches += 1
+        self._last_loss = loss
         return loss
 
     def capture(self, x: torch.Tensor, target: torch.Tensor) -> "CapturedStep":
@@ -320,7 +344,13 @@ class SplineTrainer:
             he.zero_()
         torch.cuda.current_stream(self.device).synchronize()
         v = float(hl[0])
-        if int(he[0]):
+        flag = int(he[0])
+        if flag or not math.isfinite(v):
+            if loss is getattr(self, "_last_loss", None) and self._dev_state is None:
+                self.t -= 1  # the guarded optimizer skipped this step (reference: raise before state.t += 1)
+        if flag & 2:
+            raise IndexError("label out of range for the softmax cross-entropy")
+        if flag & 1:
             raise IndexError("non-finite (NaN) input to a bounded-grid KAN layer")
         if not math.isfinite(v):
             raise DivergedError(f"non-finite loss {v}")
@@ -433,3 +463,107 @@ class DevicePrefetcher:
         self._have = self._load(prev)
         self._k = prev
         return batch
+
+
+class LayerTrainer:
+    """Data-parallel training step of ONE KAN layer inside a stack (the unit bench.py times at
+    cfg3): forward, backward INCLUDING dx (x is a recorded node: the layer below needs it, the
+    reference's tape computes it then, tensor.py:455-456), the gradient all-reduce in feature
+    buckets that overlap the rest of the backward, and one fused Adam (coupled L2) over the
+    layer's flat parameters.  Reference: the layer's share of train.step (train.py:142-150):
+    kan_forward's nodes (layers.py:304-318) + T.backward + adam_step (optim.py:31-54).
+
+    ``step(x, gy)`` takes this rank's shard and the upstream gradient dL/dy (already normalised
+    by the global batch) and returns (y, dx).  Backward order: records (x only), dx for every
+    feature, then the table gradient in ``buckets`` feature slices, each all-reduced (NCCL) as
+    soon as it is enqueued, so slice s's all-reduce runs while slice s+1 is computed."""
+
+    def __init__(self, layer: KanLayer, lr: float, weight_decay: float = 0.0, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8, buckets: int = 8, group=None):
+        if not isinstance(layer, KanLayer) or layer.base_weight is not None:
+            raise ConfigError("LayerTrainer covers KAN layers without the base branch")
+        self.lib = _lib.load()
+        self.layer = layer
+        self.model = Model("kan", [layer])
+        self.flat = FlatParams(self.model)
+        self.sync = GradSync(group)
+        self.lr, self.wd, self.beta1, self.beta2, self.eps = lr, weight_decay, beta1, beta2, eps
+        self.m = torch.zeros_like(self.flat.data)
+        self.v = torch.zeros_like(self.flat.data)
+        self.t = 0
+        self.buckets = max(1, int(buckets))
+        self.device = self.flat.data.device
+        self.timers = None  # optional {phase: [(start, end), ...]}
+        self._ws = {}
+
+    def _workspace(self, kind: str, nbytes: int):
+        buf = self._ws.get(kind)
+        if nbytes <= 0:
+            return None, 0
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, device=self.device, dtype=torch.uint8)
+            self._ws[kind] = buf
+        return buf, nbytes
+
+    def _mark(self, name):
+        return SplineTrainer._mark(self, name)
+
+    def step(self, x: torch.Tensor, gy: torch.Tensor, lr: float | None = None):
+        L = self.layer
+        if x.dim() != 2 or x.shape[1] != L.d_in:
+            raise DimensionError(f"x must be [B, {L.d_in}], got {tuple(x.shape)}")
+        if gy.shape != (x.shape[0], L.d_out):
+            raise DimensionError(f"gy must be [{x.shape[0]}, {L.d_out}], got {tuple(gy.shape)}")
+        x = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
+        gy = gy if (gy.dtype == torch.float32 and gy.is_contiguous()) else gy.float().contiguous()
+        st = stream_ptr()
+        B = x.shape[0]
+        args = (B, L.d_in, L.d_out, L.G, L.k)
+        grid = (float(L.g_min), float(L.g_max))
+        if getattr(self, "_err", None) is None:
+            self._err = torch.zeros(1, device=self.device, dtype=torch.int32)
+        y = torch.empty((B, L.d_out), device=self.device, dtype=torch.float32)
+        dx = torch.empty_like(x)
+        gv = self.flat.gviews
+        dC, dS = gv["layer0.coeffs"], gv["layer0.scale"]
+        with self._mark("forward"):
+            wsf, nf = self._workspace("fwd", self.lib.ukan_kan_forward_workspace_size(*args))
+            check(self.lib.ukan_kan_forward_ws(ptr(x), ptr(L.coeffs), ptr(L.scale), None, ptr(y), *args, *grid,
+                                               ptr(self._err), ptr(wsf), nf, st), "kan_forward")
+        wsb, nb = self._workspace("bwd", self.lib.ukan_kan_backward_workspace_size(*args))
+        if B > 0 and self.lib.ukan_kan_backward_part_supported(*args):
+            with self._mark("backward_prep"):
+                prepared = ctypes.c_int32(0)
+                check(self.lib.ukan_kan_backward_prep(ptr(x), None, *args, *grid, ptr(wsb), nb, ctypes.byref(prepared),
+                                                      st), "kan_backward_prep")
+            with self._mark("backward_dx"):
+                check(self.lib.ukan_kan_backward_part(ptr(L.coeffs), ptr(L.scale), ptr(gy), ptr(dx), None, None, *args,
+                                                      *grid, ptr(wsb), nb, 0, L.d_in, 2, st), "kan_backward_dx")
+            bounds = [round(L.d_in * q / self.buckets) for q in range(self.buckets + 1)]
+            with self._mark("backward_table"):
+                for lo, hi in zip(bounds[:-1], bounds[1:]):
+                    if hi <= lo:
+                        continue
+                    check(self.lib.ukan_kan_backward_part(ptr(L.coeffs), ptr(L.scale), ptr(gy), None, ptr(dC), ptr(dS),
+                                                          *args, *grid, ptr(wsb), nb, lo, hi, 1, st),
+                          "kan_backward_table")
+                    self.sync.allreduce_async(dC[lo:hi])
+                    self.sync.allreduce_async(dS[lo:hi])
+        else:
+            with self._mark("backward"):
+                check(self.lib.ukan_kan_backward_ws2(ptr(x), ptr(L.coeffs), ptr(L.scale), None, ptr(gy), ptr(dx),
+                                                     ptr(dC), ptr(dS), None, *args, *grid, ptr(wsb), nb, 0, st),
+                      "kan_backward")
+            self.sync.allreduce_async(self.flat.grad)
+        self.sync.wait()
+        self.t += 1
+        with self._mark("adam"):
+            check(self.lib.ukan_adam_step(ptr(self.flat.data), ptr(self.flat.grad), ptr(self.m), ptr(self.v),
+                                          self.flat.data.numel(), self.lr if lr is None else lr, self.beta1,
+                                          self.beta2, self.eps, self.wd, self.t, None, st), "adam")
+        return y, dx
+
+    def check_input(self) -> None:
+        """Host read of the NaN flag of the steps so far (the reference raises IndexError)."""
+        if getattr(self, "_err", None) is not None and int(self._err.item()):
+            raise IndexError("non-finite (NaN) input to a bounded-grid KAN layer")

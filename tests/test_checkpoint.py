@@ -20,7 +20,7 @@ def test_reads_reference_checkpoint_and_rewrites_identically(tmp_path):
     assert "model = kan" in cfg and "widths = 3,4,2" in cfg
     assert list(tensors) == ["layer0.coeffs", "layer0.scale", "layer1.coeffs", "layer1.scale"]
     out = tmp_path / "again.ukanckp"
-    ck.save_checkpoint(str(out), tensors, meta, cfg)
+    ck.save_checkpoint(str(out), cfg, tensors, meta)
     assert out.read_bytes() == open(REF_CKPT, "rb").read()
 
 
@@ -32,9 +32,14 @@ def test_model_roundtrip_through_reference_format(tmp_path):
     for n in tensors:
         np.testing.assert_array_equal(state[n], tensors[n])   # values are fp32-representable
     p = tmp_path / "m.ukanckp"
-    ck.save_checkpoint(str(p), state, {"epoch": 1})
-    _, t2, m2 = ck.load_checkpoint(str(p))
+    ck.save_checkpoint(str(p), model, state, {"epoch": 1})
+    cfg2, t2, m2 = ck.load_checkpoint(str(p))
     assert m2 == {"epoch": 1} and all(np.array_equal(t2[n], state[n]) for n in state)
+    # the echo rebuilds the same architecture in the reference's config format
+    assert "model = kan\n" in cfg2 and "widths = 3,4,2\n" in cfg2 and "grid_size = 6\n" in cfg2
+    assert "degree = 3\n" in cfg2 and cfg2.startswith("task = ")
+    with pytest.raises(P.ConfigError):
+        ck.save_checkpoint(str(p), None, state, {})
 
 
 def test_format_errors(tmp_path):
@@ -53,3 +58,6 @@ def test_format_errors(tmp_path):
     _, tensors, _ = ck.load_checkpoint(REF_CKPT)
     with pytest.raises(FormatError):
         ck.load_model_state(model, tensors)
+    model = P.build_model("kan", [3, 4, 2], 3, seed=0, G=6, device="cpu")
+    with pytest.raises(FormatError):  # extra names are rejected, as the reference does
+        ck.load_model_state(model, {**tensors, "layer2.coeffs": tensors["layer0.coeffs"]})

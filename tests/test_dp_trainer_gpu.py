@@ -1,0 +1,90 @@
+"""SplineTrainer.step with world size 2 (reference step: train.py:142-150): two
+ranks over gloo sharing cuda:0 (this run has one GPU; the bench's N > 1 path is the same code
+over NCCL), UNEVEN contiguous shards, n_global NOT passed (the trainer all-reduces the shard
+sizes).  The summed gradients, the all-reduced loss and the Adam-updated parameters of rank 0
+must equal a single-process step over the whole batch (rtol 1e-5 / atol 1e-6: the all-reduce
+order changes fp32 rounding)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import assert_close
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "kan": dict(widths=[16, 24, 5], kw=dict(g_min=-1.0, g_max=1.0, G=8), loss="softmax_cross_entropy"),
+    "ukan": dict(widths=[6, 8, 3], kw=dict(delta_g=0.5, d_pe=8, d_femb=8), loss="mse"),
+}
+B = 37  # shards 19 + 18
+
+
+def _data(kind):
+    rng = np.random.default_rng(5)
+    c = CASES[kind]
+    x = (rng.uniform(-1.2, 1.2, (B, c["widths"][0])) if kind == "kan"
+         else rng.normal(0, 3.0, (B, c["widths"][0]))).astype(np.float32)
+    if c["loss"] == "mse":
+        t = rng.normal(size=(B, c["widths"][-1])).astype(np.float32)
+    else:
+        t = rng.integers(0, c["widths"][-1], B)
+    return x, t
+
+
+def _run(kind, x, t, group_world=1, rank=0):
+    import paper_2408_11200_b200 as P
+    from paper_2408_11200_b200.train import shard_bounds
+    c = CASES[kind]
+    model = P.build_model(kind, c["widths"], 3, seed=0, device="cuda", **c["kw"])
+    tr = P.SplineTrainer(model, c["loss"], 1e-2, "adam")
+    lo, hi = shard_bounds(B, rank, group_world)
+    xs = torch.tensor(x[lo:hi], device="cuda")
+    ts = torch.tensor(t[lo:hi], device="cuda")
+    loss = tr.read_loss(tr.step(xs, ts))
+    return loss, tr.flat.grad.cpu().numpy().copy(), tr.flat.data.cpu().numpy().copy()
+
+
+def _worker(rank, world, port, kind, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, t = _data(kind)
+        out = _run(kind, x, t, world, rank)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("kind", ["kan", "ukan"])
+def test_two_ranks_uneven_shards_match_single_process(kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    x, t = _data(kind)
+    loss1, grad1, data1 = _run(kind, x, t)
+    for r in (0, 1):
+        loss2, grad2, data2 = res[r]
+        assert abs(loss2 - loss1) <= 1e-6 + 1e-5 * abs(loss1)
+        assert_close(grad2, grad1, what=f"rank{r} summed gradient")
+        assert_close(data2, data1, what=f"rank{r} updated parameters")
+    # both ranks hold identical replicas after the step
+    np.testing.assert_array_equal(res[0][2], res[1][2])
