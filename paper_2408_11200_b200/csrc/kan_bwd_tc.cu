@@ -169,7 +169,10 @@ kan_bwd_tc_sweep_kernel(const unsigned char* __restrict__ recs, const float* __r
   const int R = G + 3;
   const size_t rb = tc_rec_bytes(G);
   __shared__ double Msh[16];  // basis matrix (dynamic column index -> shared, not local memory)
-  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  if (threadIdx.x == 0) {  // constant indices: no local-memory copy of the parameter struct
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Msh[q] = bas.M[q / 4][q % 4];
+  }
   unsigned char* rec_s = smem_raw;                                            // 2 x [8][rb]
   float* g_s = reinterpret_cast<float*>(smem_raw + 2 * 8 * rb);               // 2 x [BC][OPB]
 
@@ -308,15 +311,33 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, kq = lane & 3;
   const int fl = warp / WPF, h = warp % WPF;
-  const int i0 = blockIdx.y * FPB;  // output tiles fastest: the CTAs sharing a feature group's records run together
+  // Grid walk in panels of kSwFG feature groups x all output tiles, feature group fastest inside a
+  // panel: a wave of resident CTAs covers ~148/kSwFG output tiles x kSwFG feature groups, so it
+  // shares both the g columns of its output tiles and the records of its feature groups through L2
+  // (row-major order re-read all of g once per feature group: 244 GB per call at cfg3, B = 16384).
+  constexpr int kSwFG = 16;
+  int ot, fg;
+  {
+    const int n_ot = gridDim.x, n_fg = gridDim.y;
+    const int L = blockIdx.y * n_ot + blockIdx.x;
+    const int pw = min(kSwFG, n_fg);
+    const int sc = L / (pw * n_ot), r = L % (pw * n_ot);
+    const int pe = min(pw, n_fg - sc * pw);
+    ot = r / pe;
+    fg = sc * pw + r % pe;
+  }
+  const int i0 = fg * FPB;
   const int i = i0 + fl;
-  const int o0 = blockIdx.x * OPB;
+  const int o0 = ot * OPB;
   const int z = blockIdx.z;
   const int n_lo = z * cps, n_hi = min(nch, n_lo + cps);
   const int R = G + 3;
   const size_t rb = tc_rec_bytes(G);
   __shared__ double Msh[16];
-  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  if (threadIdx.x == 0) {  // constant indices: no local-memory copy of the parameter struct
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Msh[q] = bas.M[q / 4][q % 4];
+  }
   unsigned char* rec_s = smem_raw;                                              // 2 x [FPB][rb]
   float* g_s = reinterpret_cast<float*>(smem_raw + 2 * FPB * rb);               // 2 x [BC][OPB]
   double* w_s = reinterpret_cast<double*>(g_s + (size_t)2 * kTcBC * GST);       // [FPB][BC][4] basis weights
@@ -378,26 +399,52 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
       const double* wf = w_s + (size_t)fl * kTcBC * 4;
       const int* ent = reinterpret_cast<const int*>(rec);
       const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
-      const float* gl = g_s + (size_t)buf * kTcBC * GST + grp;
+      // B operand: lane (sample kq, column n = grp) of tile t is output o0 + n*NT + t, so a lane's NT
+      // values are contiguous (LDS.128); the epilogue maps the columns back
+      const float* gl = g_s + (size_t)buf * kTcBC * GST + grp * NT;
+      // one group = 4 consecutive sorted samples (the k = 4 operand); invalid positions read a real
+      // (zero-filled or other) sample row and are masked by a = 0
+      auto load_group = [&](int kc, int e1, double& a, float4 (&gv)[NT / 4]) {
+        const int pos = kc + kq;
+        const int pc = min(pos, kTcBC - 1);
+        const int e = ent[pc];
+        const int j = grp - ((e >> 8) & 3);
+        const double wj = wf[pc * 4 + (j & 3)];
+        a = (pos < e1 && j >= 0 && j < 4) ? wj : 0.0;
+        const float* gp = gl + (e & 255) * GST;
+#pragma unroll
+        for (int q = 0; q < NT / 4; ++q) gv[q] = *reinterpret_cast<const float4*>(gp + 4 * q);
+      };
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
         const int bb = h * BH + bl;
         const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
-#pragma unroll 4
-        for (int kc = e0; kc < e1; kc += 4) {
-          const int pos = kc + kq;
-          const bool vld = pos < e1;
-          const int pc = min(pos, kTcBC - 1);
-          const int e = ent[pc];
-          const int j = grp - ((e >> 8) & 3);
-          const double wj = wf[pc * 4 + (j & 3)];
-          const double a = (vld && j >= 0 && j < 4) ? wj : 0.0;
-          const int srow = (e & 255) * GST;
-          double bf[NT];  // rows of invalid positions are real (zero-filled) samples: a = 0 masks them
+        int kc = e0;
+        for (; kc + 4 < e1; kc += 8) {  // two groups in flight
+          double a0, a1;
+          float4 g0[NT / 4], g1[NT / 4];
+          load_group(kc, e1, a0, g0);
+          load_group(kc + 4, e1, a1, g1);
 #pragma unroll
-          for (int t = 0; t < NT; ++t) bf[t] = (double)gl[srow + t * 8];
+          for (int t = 0; t < NT; ++t) {
+            const float v0 = t % 4 == 0 ? g0[t / 4].x : t % 4 == 1 ? g0[t / 4].y : t % 4 == 2 ? g0[t / 4].z : g0[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a0, (double)v0);
+          }
 #pragma unroll
-          for (int t = 0; t < NT; ++t) tc_dmma(acc[bl][t][0], acc[bl][t][1], a, bf[t]);
+          for (int t = 0; t < NT; ++t) {
+            const float v1 = t % 4 == 0 ? g1[t / 4].x : t % 4 == 1 ? g1[t / 4].y : t % 4 == 2 ? g1[t / 4].z : g1[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a1, (double)v1);
+          }
+        }
+        if (kc < e1) {
+          double a0;
+          float4 g0[NT / 4];
+          load_group(kc, e1, a0, g0);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float v0 = t % 4 == 0 ? g0[t / 4].x : t % 4 == 1 ? g0[t / 4].y : t % 4 == 2 ? g0[t / 4].z : g0[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a0, (double)v0);
+          }
         }
       }
     }
@@ -417,7 +464,7 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
-          for (int v = 0; v < 2; ++v) S[((size_t)fl * RR + r) * OPB + t * 8 + 2 * kq + v] += acc[bl][t][v];
+          for (int v = 0; v < 2; ++v) S[((size_t)fl * RR + r) * OPB + (2 * kq + v) * NT + t] += acc[bl][t][v];
         __syncwarp();
       }
     }
@@ -518,6 +565,16 @@ TcPlan kan_bwd_tc_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
     p.nt = 4;
     p.fpb = 4;
   }
+  if (p.split && p.rb == 16 && rb16_wpf == 8 && d_out >= 64) {  // 16 warps: 2 features x 8 block parts, NT = 8
+    p.wpf = 8;
+    p.nt = 8;
+    p.fpb = 2;
+  }
+  if (p.split && p.rb == 16 && rb16_wpf == 84) {  // 32 warps: 4 features x 8 block parts, NT = 4 (64 registers)
+    p.wpf = 8;
+    p.nt = 4;
+    p.fpb = 4;
+  }
   const int opb = 8 * p.nt;
   const int fpb = p.split ? p.fpb : 8;
   p.nch = (int)((B + kTcBC - 1) / kTcBC);
@@ -604,6 +661,8 @@ static int tc_sweep_dispatch(const float* C, const float* scale, const float* gy
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 4) return tc2_launch<16, 4, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16 && p.wpf == 8 && p.fpb == 2) return tc2_launch<16, 8, 2, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 16 && p.wpf == 8) return tc2_launch<16, 4, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16) return tc2_launch<16, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 1) return tc_launch<4, 1>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.rb == 4 && p.nt == 2) return tc_launch<4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
@@ -646,12 +705,13 @@ int kan_bwd_tc_run(const float* x, const float* C, const float* scale, const flo
 // band's g rows and a few features' C' through L2.  Deterministic: fixed task order, fixed DMMA
 // order over the outputs, fixed 4-lane reduction.
 // ---------------------------------------------------------------------------------------
-constexpr int kDxF = 4;            // features per CTA
-constexpr int kDxW = 16;           // warps per CTA
+constexpr int kDxF = 4;            // features per CTA (task_at below is written for 4)
 constexpr int kDxOT = 16;          // outputs per staged tile
 constexpr int kDxGS = kDxOT;       // fp32 g row stride (floats, 64 B): a row's bank half = sample & 1
 constexpr int kDxCS = kDxOT + 2;   // fp64 C' row stride (doubles, 144 B): adjacent rows on disjoint banks
-constexpr int kDxMaxT = 12;        // tasks per warp: 4 * (256/8 + G/5 + 1) / 16 <= 12 for G <= 64
+// warps per CTA NW and task slots per warp MAXT: tasks per CTA <= 4 * (256/8 + G/5 + 1) <= 184 for G <= 64,
+// so 16 warps need 12 slots, 32 warps 6 (fewer registers per thread, twice the warps per scheduler)
+constexpr int kDxMaxT = 12;
 constexpr int kDxTPF = 48;         // task slots per feature (>= 256/8 + 64/5 + 1)
 
 __host__ __device__ constexpr int dx_rr(int G) { return G + 8; }  // C' tile rows: c0 + 7 <= G + 6
@@ -700,22 +760,41 @@ __device__ __forceinline__ int dx_lane_pos(const int* ent, int p0, int p1, int g
 // One staged output tile for NT tasks: per task one LDS.128 of A (4 fp32 g values of this lane's
 // sample) and two LDS.128 of B (4 fp64 C' values of row c0 + grp), then 4 DMMAs.  The k slot of
 // lane kq in DMMA kk is output 4*kq + kk (any fixed k order is valid: A and B use the same one).
-template <int NT>
+template <int NT, int MAXT>
 __device__ __forceinline__ void dx_tile(const float* __restrict__ gb, const double* __restrict__ cb,
-                                        const uint32_t (&toff)[kDxMaxT], double (&acc)[kDxMaxT][2]) {
+                                        const uint32_t (&toff)[MAXT], double (&acc)[MAXT][2]) {
+  // tasks in pairs: both tasks' operands are loaded before either DMMA chain starts and the two
+  // accumulator chains interleave (the A operand's LDS -> F2F -> DMMA latency overlaps)
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {  // straight-line: ptxas hoists the loads of later tasks as registers allow
-    const float4 a = *reinterpret_cast<const float4*>(gb + (toff[t] & 0xffffu));
-    const double* cp = cb + (toff[t] >> 16);
-    const double2 b0 = *reinterpret_cast<const double2*>(cp);
-    const double2 b1 = *reinterpret_cast<const double2*>(cp + 2);
-    tc_dmma(acc[t][0], acc[t][1], (double)a.x, b0.x);
-    tc_dmma(acc[t][0], acc[t][1], (double)a.y, b0.y);
-    tc_dmma(acc[t][0], acc[t][1], (double)a.z, b1.x);
-    tc_dmma(acc[t][0], acc[t][1], (double)a.w, b1.y);
+  for (int t0 = 0; t0 < NT; t0 += 2) {
+    constexpr int W = 2;
+    float4 a[W];
+    double2 b0[W], b1[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      if (t0 + u < NT) {
+        a[u] = *reinterpret_cast<const float4*>(gb + (toff[t0 + u] & 0xffffu));
+        const double* cp = cb + (toff[t0 + u] >> 16);
+        b0[u] = *reinterpret_cast<const double2*>(cp);
+        b1[u] = *reinterpret_cast<const double2*>(cp + 2);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+      if (t0 + u < NT) tc_dmma(acc[t0 + u][0], acc[t0 + u][1], (double)a[u].x, b0[u].x);
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+      if (t0 + u < NT) tc_dmma(acc[t0 + u][0], acc[t0 + u][1], (double)a[u].y, b0[u].y);
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+      if (t0 + u < NT) tc_dmma(acc[t0 + u][0], acc[t0 + u][1], (double)a[u].z, b1[u].x);
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+      if (t0 + u < NT) tc_dmma(acc[t0 + u][0], acc[t0 + u][1], (double)a[u].w, b1[u].y);
   }
 }
 
+template <int kDxW, int MAXT>
 __global__ void __launch_bounds__(kDxW * 32, 1)
 kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C, const float* __restrict__ scale,
                  const float* __restrict__ gy, float* __restrict__ dx, int B, int d_in, int d_out, int G, int nch,
@@ -728,6 +807,10 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   const int grp = lane >> 2, kq = lane & 3;
   const int R = G + 3, RR = dx_rr(G);
   const size_t rb = tc_rec_bytes(G);
+  if (threadIdx.x == 0) {  // constant indices: no local-memory copy of the parameter struct
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Msh[q] = bas.M[q / 4][q % 4];
+  }
   // banded walk: band b covers chunks [b*band, ...) x all feature groups, feature group major
   const int64_t lin = blockIdx.x;
   const int64_t per_band = (int64_t)band * n_fg;
@@ -744,7 +827,7 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   double* c_s = reinterpret_cast<double*>(smem_raw + L.c);
   float* dx_s = reinterpret_cast<float*>(smem_raw + L.dxs);
   const int GSZ = (kTcBC + 1) * kDxGS, CSZ = kDxF * RR * kDxCS;
-  if (threadIdx.x < 16) Msh[threadIdx.x] = bas.M[threadIdx.x / 4][threadIdx.x % 4];
+  
   // records of the 4 features (16-byte granules)
   {
     const int q = (int)(rb / 16);
@@ -819,25 +902,19 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
     cnt_s[f] = cnt;
   }
   __syncthreads();
-  int T = 0, base_f[kDxF];
-#pragma unroll
-  for (int f = 0; f < kDxF; ++f) {
-    base_f[f] = T;
-    T += cnt_s[f];
-  }
+  const int T = cnt_s[0] + cnt_s[1] + cnt_s[2] + cnt_s[3];
   const int per = (T + kDxW - 1) / kDxW;
   const int t_lo = min(T, warp * per), nt = min(per, T - t_lo);
   // per task: packed smem offsets (A: g row of this lane's sample, B: C' row c0 + grp)
-  auto task_at = [&](int gt) {  // global task index -> its record (feature-major order)
-    int f = 0;
-#pragma unroll
-    for (int ff = 1; ff < kDxF; ++ff)
-      if (gt >= base_f[ff]) f = ff;
-    return task_s[f * kDxTPF + gt - base_f[f]];
+  auto task_at = [&](int gt) {  // global task index -> its record (feature-major order), no local arrays
+    const int c0 = cnt_s[0], c1 = c0 + cnt_s[1], c2 = c1 + cnt_s[2];
+    const int f = gt >= c2 ? 3 : (gt >= c1 ? 2 : (gt >= c0 ? 1 : 0));
+    const int base = f == 3 ? c2 : (f == 2 ? c1 : (f == 1 ? c0 : 0));
+    return task_s[f * kDxTPF + gt - base];
   };
-  uint32_t toff[kDxMaxT];
+  uint32_t toff[MAXT];
 #pragma unroll
-  for (int t = 0; t < kDxMaxT; ++t) {
+  for (int t = 0; t < MAXT; ++t) {
     toff[t] = 0;
     if (t < nt) {
       const int4 ti = task_at(t_lo + t);
@@ -848,9 +925,9 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
       toff[t] = (uint32_t)(sm * kDxGS + 4 * kq) | ((uint32_t)((f * RR + ti.y + grp) * kDxCS + 4 * kq) << 16);
     }
   }
-  double acc[kDxMaxT][2];
+  double acc[MAXT][2];
 #pragma unroll
-  for (int t = 0; t < kDxMaxT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  for (int t = 0; t < MAXT; ++t) acc[t][0] = acc[t][1] = 0.0;
   for (int ot = 0; ot < n_ot; ++ot) {
     const int buf = ot & 1;
     const bool more = ot + 1 < n_ot;
@@ -862,19 +939,25 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
     const float* gb = g_s + buf * GSZ;
     const double* cbuf = c_s + buf * CSZ;
     switch (nt) {  // warp-uniform: a fully unrolled, predicate-free body per task count
-      case 1: dx_tile<1>(gb, cbuf, toff, acc); break;
-      case 2: dx_tile<2>(gb, cbuf, toff, acc); break;
-      case 3: dx_tile<3>(gb, cbuf, toff, acc); break;
-      case 4: dx_tile<4>(gb, cbuf, toff, acc); break;
-      case 5: dx_tile<5>(gb, cbuf, toff, acc); break;
-      case 6: dx_tile<6>(gb, cbuf, toff, acc); break;
-      case 7: dx_tile<7>(gb, cbuf, toff, acc); break;
-      case 8: dx_tile<8>(gb, cbuf, toff, acc); break;
-      case 9: dx_tile<9>(gb, cbuf, toff, acc); break;
-      case 10: dx_tile<10>(gb, cbuf, toff, acc); break;
-      case 11: dx_tile<11>(gb, cbuf, toff, acc); break;
-      case 12: dx_tile<12>(gb, cbuf, toff, acc); break;
-      default: break;
+      case 1: dx_tile<1, MAXT>(gb, cbuf, toff, acc); break;
+      case 2: dx_tile<2, MAXT>(gb, cbuf, toff, acc); break;
+      case 3: dx_tile<3, MAXT>(gb, cbuf, toff, acc); break;
+      case 4: dx_tile<4, MAXT>(gb, cbuf, toff, acc); break;
+      case 5: dx_tile<5, MAXT>(gb, cbuf, toff, acc); break;
+      case 6: dx_tile<6, MAXT>(gb, cbuf, toff, acc); break;
+      default:
+        if constexpr (MAXT > 6) {
+          switch (nt) {
+            case 7: dx_tile<7, MAXT>(gb, cbuf, toff, acc); break;
+            case 8: dx_tile<8, MAXT>(gb, cbuf, toff, acc); break;
+            case 9: dx_tile<9, MAXT>(gb, cbuf, toff, acc); break;
+            case 10: dx_tile<10, MAXT>(gb, cbuf, toff, acc); break;
+            case 11: dx_tile<11, MAXT>(gb, cbuf, toff, acc); break;
+            case 12: dx_tile<12, MAXT>(gb, cbuf, toff, acc); break;
+            default: break;
+          }
+        }
+        break;
     }
     if (more) {
       store_c((ot + 1) * kDxOT, buf ^ 1);
@@ -884,7 +967,7 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   }
   // epilogue: lane (grp, kq) holds Q[sample grp][rows c0 + 2kq, c0 + 2kq + 1]
 #pragma unroll
-  for (int t = 0; t < kDxMaxT; ++t) {
+  for (int t = 0; t < MAXT; ++t) {
     if (t < nt) {
       const int4 ti = task_at(t_lo + t);
       const int f = ti.x;
@@ -927,13 +1010,24 @@ bool kan_dx_tc_applicable(const TcPlan& p, const float* C, const float* gy, int 
 static int dx_tc_launch(const float* C, const float* scale, const float* gy, float* dx, const unsigned char* recs,
                         int B, int d_in, int d_out, int G, int nch, int ld, const KanGrid& grid, cudaStream_t st) {
   const DxSmem L = dx_smem_layout(G);
-  UKAN_CUDA_TRY(cudaFuncSetAttribute(kan_dx_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   const int n_fg = (d_in + kDxF - 1) / kDxF;
-  static const int band_env = getenv("UKAN_DX_BAND") ? atoi(getenv("UKAN_DX_BAND")) : 16;
+  // band 8: least DRAM traffic at cfg3 (45.8 GB per call at B = 16384 vs 72 GB at 16, 192 GB at 32;
+  // time unchanged); 16 warps x 12 tasks measured faster than 32 x 6 (64 registers spill)
+  static const int band_env = getenv("UKAN_DX_BAND") ? atoi(getenv("UKAN_DX_BAND")) : 8;
+  static const int warps_env = getenv("UKAN_DX_WARPS") ? atoi(getenv("UKAN_DX_WARPS")) : 16;
   const int band = std::max(1, std::min(band_env, nch));
   const int64_t nblk = (int64_t)nch * n_fg;
-  kan_dx_tc_kernel<<<(unsigned)nblk, kDxW * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg,
-                                                                band, ld, grid.inv_dg, make_basis<4>(3));
+  if (warps_env == 16) {
+    auto kern = kan_dx_tc_kernel<16, 12>;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    kern<<<(unsigned)nblk, 16 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
+                                                   grid.inv_dg, make_basis<4>(3));
+  } else {
+    auto kern = kan_dx_tc_kernel<32, 6>;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    kern<<<(unsigned)nblk, 32 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
+                                                   grid.inv_dg, make_basis<4>(3));
+  }
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }
