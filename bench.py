@@ -191,7 +191,9 @@ def _cpu_procs():
         mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
     except (ValueError, OSError):
         mem_gb = 64
-    return max(1, min(ncpu, int(mem_gb // 16)))  # ~15 GB peak per process at B = 4 (zeros_like table)
+    # per process: the layer's float64 coefficients (9 GB) + zeros_like(table) in span_gather's
+    # backward (9 GB) + windows / einsum temporaries at B = 4 (~5 GB)
+    return max(1, min(ncpu, int(mem_gb // 28)))
 
 
 def reference_arm(args, rank):

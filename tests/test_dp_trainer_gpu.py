@@ -88,3 +88,75 @@ def test_two_ranks_uneven_shards_match_single_process(kind):
         assert_close(data2, data1, what=f"rank{r} updated parameters")
     # both ranks hold identical replicas after the step
     np.testing.assert_array_equal(res[0][2], res[1][2])
+
+
+def _layer_run(x, gy, world=1, rank=0, buckets=3):
+    import paper_2408_11200_b200 as P
+    from paper_2408_11200_b200.train import shard_bounds
+    layer = P.init_layer("kan", 24, 64, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
+    tr = P.LayerTrainer(layer, 1e-2, buckets=buckets)
+    lo, hi = shard_bounds(x.shape[0], rank, world)
+    y, dx = tr.step(torch.tensor(x[lo:hi], device="cuda"), torch.tensor(gy[lo:hi], device="cuda"))
+    torch.cuda.synchronize()
+    return (y.cpu().numpy(), dx.cpu().numpy(), tr.flat.grad.cpu().numpy().copy(), tr.flat.data.cpu().numpy().copy())
+
+
+def _layer_data():
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1.2, 1.2, (301, 24)).astype(np.float32)
+    gy = (rng.normal(size=(301, 64)) / 301).astype(np.float32)  # dL/dy of a global mean loss
+    return x, gy
+
+
+def _layer_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, gy = _layer_data()
+        q.put((rank, _layer_run(x, gy, world, rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_layer_trainer_matches_autograd_and_oracle():
+    """LayerTrainer (the bench's cfg3 unit: dx first, then the table gradient in feature buckets
+    via ukan_kan_backward_part) against the drop-in autograd path and the oracle."""
+    import oracle
+    import paper_2408_11200_b200 as P
+    x, gy = _layer_data()
+    y, dx, grad, _ = _layer_run(x, gy, buckets=3)
+    layer = P.init_layer("kan", 24, 64, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
+    p = {n: t.detach().double().cpu().numpy() for n, t in layer.parameters().items()}
+    want = oracle.kan_forward_backward(x.astype(np.float64), p["coeffs"], p["scale"], gy.astype(np.float64), k=3,
+                                       g_min=-1.0, g_max=1.0, G=16)
+    assert_close(y, want["y"], what="y")
+    assert_close(dx, want["dx"], what="dx")
+    nC = p["coeffs"].size
+    assert_close(grad[:nC].reshape(p["coeffs"].shape), want["dcoeffs"], what="dcoeffs")
+    assert_close(grad[nC:].reshape(p["scale"].shape), want["dscale"], what="dscale")
+    _, _, grad1, _ = _layer_run(x, gy, buckets=1)
+    np.testing.assert_array_equal(grad, grad1)  # bucketing does not change a bit
+
+
+def test_layer_trainer_two_ranks_match_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    x, gy = _layer_data()
+    y1, dx1, grad1, data1 = _layer_run(x, gy)
+    from paper_2408_11200_b200.train import shard_bounds
+    for r in (0, 1):
+        lo, hi = shard_bounds(x.shape[0], r, 2)
+        y2, dx2, grad2, data2 = res[r]
+        np.testing.assert_array_equal(y2, y1[lo:hi])  # forward / dx are per sample: bitwise
+        np.testing.assert_array_equal(dx2, dx1[lo:hi])
+        assert_close(grad2, grad1, what=f"rank{r} summed gradient")
+    np.testing.assert_array_equal(res[0][3], res[1][3])
