@@ -191,16 +191,16 @@ def _cpu_procs():
         mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
     except (ValueError, OSError):
         mem_gb = 64
-    # per process: the layer's float64 coefficients (9 GB) + zeros_like(table) in span_gather's
-    # backward (9 GB) + windows / einsum temporaries at B = 4 (~5 GB)
-    return max(1, min(ncpu, int(mem_gb // 28)))
+    # measured peak RSS of one reference process at cfg3, B = 4: 40 GB (the float64 coefficients,
+    # zeros_like(table) in span_gather's backward and the einsum temporaries); keep 10% headroom
+    return max(1, min(ncpu, int(mem_gb // 44)))
 
 
 def reference_arm(args, rank):
     if rank != 0:
         return
     procs = _cpu_procs()
-    reps = max(1, min(2, args.steps))
+    reps = 1  # one (B=1, B=4) pair per process: ~25 s of reference work after a ~24 s layer init
     t0 = time.perf_counter()
     rate, pairs = cpu_rate(procs, reps)
     wall = time.perf_counter() - t0
@@ -330,7 +330,7 @@ def our_arm(args, rank, world, local_rank):
         if world == 1:
             supp["cfg2_kan_stack_dp"] = cfg2_rate(dev)
             supp["ukan_layer"] = ukan_layer_rate(dev)
-            supp["kan_layers"] = kan_layer_rates(dev)
+            supp["kan_layers"] = kan_layer_rates(dev)  # cfg1 (autograd API and as a captured step)
             supp["pinn"] = pinn_rate(dev)
     if rank != 0:
         return
@@ -351,7 +351,7 @@ def our_arm(args, rank, world, local_rank):
     achieved = f_pass / (dom_ms * 1e-3) / 1e12
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic_r02.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as f:
             traffic = json.load(f).get("cfg3." + dom, {}).get("dram_bytes")
     except (OSError, ValueError):
         traffic = None
@@ -376,7 +376,7 @@ def our_arm(args, rank, world, local_rank):
                    "l2": "inputs larger than L2 (x, gy 1 GiB each; two resident batches alternate)"},
         "roofline": {"bound": "tensor" if "DMMA" in peak_src else "fp32-fma", "kernel": kern, "achieved": achieved,
                      "peak": dom_peak, "unit": "TFLOP/s", "frac": achieved / dom_peak, "traffic": traffic,
-                     "traffic_unit": "bytes per launch group (ncu dram__bytes_read+write, profiles/traffic_r02.json)",
+                     "traffic_unit": "bytes per launch group (ncu dram__bytes_read+write, profiles/r02/traffic.json)",
                      "peak_source": peak_src, "algorithmic_flops_per_launch": f_pass, "avg_launch_ms": dom_ms},
         "roofline_hbm": {"bound": "hbm", "achieved": hbm / (ms_max / args.steps * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": hbm / (ms_max / args.steps * 1e-3) / 1e9 / pk["hbm_gbs"],
@@ -525,9 +525,32 @@ def kan_layer_rates(dev):
     ms = a.elapsed_time(b) / steps
     fl = kan_flops(B, d, d, 3)
     roof_ms = (fl / (FP32_TFLOPS_MEASURED * 1e12) + fl / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3
-    return {"cfg1": {"workload": "KAN layer 64->64 G=10 k=3 B=1024, fwd + parameter grads (autograd API)",
-                     "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "roof_ms": roof_ms,
-                     "roof_frac": roof_ms / ms}}
+    out = {"cfg1": {"workload": "KAN layer 64->64 G=10 k=3 B=1024, fwd + parameter grads (autograd API)",
+                    "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "roof_ms": roof_ms,
+                    "roof_frac": roof_ms / ms}}
+    # the same layer as a one-layer model's training step (MSE + Adam) captured as one CUDA graph:
+    # the autograd figure above is host / launch bound, this is the device cost of the step
+    model = P.build_model("kan", [d, d], 3, seed=0, device=dev, g_min=-1.0, g_max=1.0, G=G)
+    tr = P.SplineTrainer(model, "mse", 1e-3, "adam")
+    tgt = torch.randn((B, d), device=dev, generator=g)
+    for _ in range(3):
+        tr.read_loss(tr.step(x, tgt))
+    cap = tr.capture(x, tgt)
+    for _ in range(3):
+        tr.read_loss(cap.replay())
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(steps * 4):
+        loss = cap.replay()
+    b.record()
+    torch.cuda.synchronize()
+    tr.read_loss(loss)
+    msg = a.elapsed_time(b) / (steps * 4)
+    out["cfg1_graph_step"] = {"workload": "KAN [64,64] G=10 k=3 B=1024, MSE + Adam training step, one CUDA graph "
+                                          "(SplineTrainer.capture; no dx: single layer)",
+                              "samples_per_s": B / (msg * 1e-3), "ms_per_step": msg, "steps": steps * 4,
+                              "roof_ms": roof_ms, "roof_frac": roof_ms / msg}
+    return out
 
 
 def pinn_rate(dev, n_colloc=128, steps=50, warmup=5):

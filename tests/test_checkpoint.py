@@ -61,3 +61,23 @@ def test_format_errors(tmp_path):
     model = P.build_model("kan", [3, 4, 2], 3, seed=0, G=6, device="cpu")
     with pytest.raises(FormatError):  # extra names are rejected, as the reference does
         ck.load_model_state(model, {**tensors, "layer2.coeffs": tensors["layer0.coeffs"]})
+
+
+def test_config_echo_for_ukan_model_and_runconfig_like(tmp_path):
+    model = P.build_model("ukan", [2, 3, 1], 3, seed=0, delta_g=0.5, d_pe=6, d_femb=4, device="cpu")
+    text = ck.config_text(model)
+    assert "model = ukan\n" in text and "widths = 2,3,1\n" in text and "delta_g = 0.5\n" in text
+    assert "d_pe = 6\n" in text and "d_femb = 4\n" in text and text.endswith("out_dir = .\n")
+    from dataclasses import dataclass, field
+
+    @dataclass
+    class RunConfigLike:  # field order and widths rendering as config_to_text (config.py:130-137)
+        task: str = "regression_II"
+        model: str = "kan"
+        widths: list = field(default_factory=lambda: [2, 5, 1])
+
+    assert ck.config_text(RunConfigLike()) == "task = regression_II\nmodel = kan\nwidths = 2,5,1\n"
+    p = tmp_path / "u.ukanckp"
+    ck.save_checkpoint(str(p), model, ck.model_state(model), {"epoch": 0})
+    cfg, tensors, meta = ck.load_checkpoint(str(p))
+    assert cfg == text and list(tensors) == list(model.parameters())

@@ -120,3 +120,43 @@ def test_captured_step_learning_rate_change():
         runs.append({n: p.detach().cpu().numpy().copy() for n, p in model.parameters().items()})
     for n in runs[0]:
         np.testing.assert_allclose(runs[1][n], runs[0][n], rtol=1e-5, atol=1e-7, err_msg=n)
+
+
+def test_step_input_checks_like_the_reference():
+    """SplineTrainer.step validates its inputs the way the reference's losses do (tensor.py:368-400):
+    float64 / non-contiguous x are converted (same loss as fp32 x), a wrong width or label count is
+    a DimensionError, a label outside [0, c) an IndexError at the host read, never an OOB read."""
+    model = P.build_model("kan", [5, 7, 3], 3, seed=0, G=6)
+    tr = P.SplineTrainer(model, "softmax_cross_entropy", 0.0, "sgd")
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (16, 5))
+    y = rng.integers(0, 3, 16)
+    l32 = tr.read_loss(tr.step(torch.tensor(x, dtype=torch.float32, device="cuda"), torch.tensor(y, device="cuda")))
+    x64 = torch.tensor(x, dtype=torch.float64, device="cuda")
+    l64 = tr.read_loss(tr.step(x64, torch.tensor(y, dtype=torch.int32, device="cuda")))
+    assert l32 == l64
+    xt = torch.tensor(x.T.copy(), dtype=torch.float32, device="cuda").T  # non-contiguous view
+    assert tr.read_loss(tr.step(xt, torch.tensor(y, device="cuda"))) == l32
+    with pytest.raises(P.DimensionError):
+        tr.step(torch.zeros((16, 4), device="cuda"), torch.tensor(y, device="cuda"))
+    with pytest.raises(P.DimensionError):
+        tr.step(torch.tensor(x, dtype=torch.float32, device="cuda"), torch.tensor(y[:15], device="cuda"))
+    bad = y.copy()
+    bad[3] = 3
+    with pytest.raises(IndexError):
+        tr.read_loss(tr.step(torch.tensor(x, dtype=torch.float32, device="cuda"), torch.tensor(bad, device="cuda")))
+
+
+def test_skipped_step_does_not_advance_adam_counter():
+    """The reference raises DivergedError before adam_step bumps state.t (train.py:143-144)."""
+    model = P.build_model("kan", [3, 2], seed=0, G=4)
+    tr = P.SplineTrainer(model, "mse", 1e-2)
+    x = torch.zeros((4, 3), device="cuda")
+    ok = torch.zeros((4, 2), device="cuda")
+    tr.read_loss(tr.step(x, ok))
+    assert tr.t == 1
+    with pytest.raises(P.DivergedError):
+        tr.read_loss(tr.step(x, torch.full((4, 2), float("inf"), device="cuda")))
+    assert tr.t == 1
+    tr.read_loss(tr.step(x, ok))
+    assert tr.t == 2
