@@ -377,45 +377,36 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[bb][t][0] = acc[bb][t][1] = 0.0;
 
-  // One barrier per chunk: it publishes chunk n's staged records and g rows and retires chunk n-1
-  // (its buffer is refilled with chunk n+1 right after, overlapping chunk n's DMMAs).  Each warp
-  // evaluates the basis weights of its own blocks' samples (warp-local, no barrier needed).
   if (n_lo < n_hi) stage(n_lo, 0);
   asm volatile("cp.async.commit_group;\n" ::);
   for (int n = n_lo; n < n_hi; ++n) {
     const int buf = (n - n_lo) & 1;
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
     if (n + 1 < n_hi) stage(n + 1, buf ^ 1);
     asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    // basis weights of the chunk's sorted samples, once per CTA (fp64 Horner, layers.py:29-37)
+    for (int t = threadIdx.x; t < FPB * kTcBC; t += blockDim.x) {
+      const int f = t / kTcBC, pos = t % kTcBC;
+      const double u = reinterpret_cast<const double*>(rec_s + ((size_t)buf * FPB + f) * rb + kTcBC * 4)[pos];
+      double* wd = w_s + (size_t)t * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wd[j] = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+    }
+    __syncthreads();
     if (i < d_in) {
       const unsigned char* rec = rec_s + ((size_t)buf * FPB + fl) * rb;
-      double* wf = w_s + (size_t)fl * kTcBC * 4;
+      const double* wf = w_s + (size_t)fl * kTcBC * 4;
       const int* ent = reinterpret_cast<const int*>(rec);
       const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
-      {  // basis weights of this warp's samples (fp64 Horner, layers.py:29-37)
-        const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
-#pragma unroll
-        for (int bl = 0; bl < BH; ++bl) {
-          const int bb = h * BH + bl;
-          const int e1 = st[min(4 * bb + 4, G)];
-          for (int p = st[min(4 * bb, G)] + lane; p < e1; p += 32) {
-            const double u = uu[p];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              wf[p * 4 + j] = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
-          }
-        }
-        __syncwarp();
-      }
       // B operand: lane (sample kq, column n = grp) of tile t is output o0 + n*NT + t, so a lane's NT
       // values are contiguous (LDS.128); the epilogue maps the columns back
       const float* gl = g_s + (size_t)buf * kTcBC * GST + grp * NT;
-      // one group = 4 consecutive sorted samples (the k = 4 operand); positions past the block read
-      // its last sample again and are masked by a = 0
+      // one group = 4 consecutive sorted samples (the k = 4 operand); invalid positions read a real
+      // (zero-filled or other) sample row and are masked by a = 0
       auto load_group = [&](int kc, int e1, double& a, float4 (&gv)[NT / 4]) {
         const int pos = kc + kq;
-        const int pc = min(pos, e1 - 1);  // stay inside this warp's block (its weights are warp-local)
+        const int pc = min(pos, kTcBC - 1);
         const int e = ent[pc];
         const int j = grp - ((e >> 8) & 3);
         const double wj = wf[pc * 4 + (j & 3)];
@@ -457,8 +448,8 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
         }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();  // every warp is done with the staging buffers before the epilogue reuses them
   // epilogue: rows of both halves meet in S[FPB][R][OPB] (fp64, reuses the staging space)
   double* S = reinterpret_cast<double*>(smem_raw);
   const int RR = 4 * RB + 4;
