@@ -8,7 +8,7 @@
 // `mma.sync.m8n8k4.f64`: fp32 operands are widened exactly when staged, products and sums are
 // fp64 — the same arithmetic as the CUDA-core fp64 kernels they replace, ~10x faster.
 //
-// CTA = 8 warps, 128 x 64 output tile (warp tile 32 x 32 = 4 x 4 DMMA tiles, fp64 accumulators in
+// CTA = 16 warps, 128 x 128 output tile (warp tile 32 x 32 = 4 x 4 DMMA tiles, fp64 accumulators in
 // registers), K staged in chunks of 32 (fp64, padded rows -> conflict-free fragment loads),
 // double-buffered with cp.async-free register staging (global fp32 -> registers -> fp64 smem).
 // Long reductions are split over blockIdx.z into fp64 partials reduced in fixed order.
@@ -18,10 +18,11 @@
 
 namespace ukan {
 
-constexpr int kDgM = 128, kDgN = 64, kDgK = 32;
+constexpr int kDgM = 128, kDgN = 128, kDgK = 32;
 constexpr int kDgAS = kDgK + 4;   // As[m][k] row stride (doubles): 288 B rows -> 2 wavefronts per fragment
 constexpr int kDgBS = kDgN + 4;   // Bs[k][n] row stride (doubles)
-constexpr int kDgThreads = 256;
+constexpr int kDgThreads = 512;  // 16 warps (4 x 4 warp tiles of 32 x 32): twice the warps per SM of the 8-warp
+                                  // 128 x 64 version (latency-bound at 12% warps active), each operand fragment used 4x
 
 __device__ __forceinline__ void dg_dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -55,13 +56,13 @@ cg_dmma_gemm_kernel(const TA* __restrict__ A, int64_t sam, int64_t sak, const TB
   const int kb = z * kps, ke = min(K, kb + kps);
   const int nch = (ke - kb + kDgK - 1) / kDgK;
 
-  // staging registers: A chunk 128 x 32 = 16 / thread, B chunk 32 x 64 = 8 / thread
-  TA ra[16];
+  // staging registers: A chunk 128 x 32 = 8 / thread, B chunk 32 x 128 = 8 / thread
+  TA ra[8];
   TB rb[8];
   auto fetch = [&](int c) {
     const int k0 = kb + c * kDgK;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int q = 0; q < 8; ++q) {
       const int e = threadIdx.x + q * kDgThreads;  // element of the 128 x 32 chunk
       int m, k;
       if (sak == 1) { m = e >> 5; k = e & 31; } else { k = e >> 7; m = e & 127; }  // walk the contiguous dim
@@ -70,9 +71,9 @@ cg_dmma_gemm_kernel(const TA* __restrict__ A, int64_t sam, int64_t sak, const TB
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int e = threadIdx.x + q * kDgThreads;  // element of the 32 x 64 chunk
+      const int e = threadIdx.x + q * kDgThreads;  // element of the 32 x 128 chunk
       int n, k;
-      if (sbk == 1) { n = e >> 5; k = e & 31; } else { k = e >> 6; n = e & 63; }
+      if (sbk == 1) { n = e >> 5; k = e & 31; } else { k = e >> 7; n = e & 127; }
       const int gn = n0 + n, gk = k0 + k;
       rb[q] = (gn < N && gk < ke) ? __ldg(Bm + (size_t)gk * sbk + (size_t)gn * sbn) : (TB)0;
     }
@@ -81,7 +82,7 @@ cg_dmma_gemm_kernel(const TA* __restrict__ A, int64_t sam, int64_t sak, const TB
     double* as = As + buf * kDgM * kDgAS;
     double* bs = Bs + buf * kDgK * kDgBS;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int q = 0; q < 8; ++q) {
       const int e = threadIdx.x + q * kDgThreads;
       int m, k;
       if (sak == 1) { m = e >> 5; k = e & 31; } else { k = e >> 7; m = e & 127; }
@@ -91,7 +92,7 @@ cg_dmma_gemm_kernel(const TA* __restrict__ A, int64_t sam, int64_t sak, const TB
     for (int q = 0; q < 8; ++q) {
       const int e = threadIdx.x + q * kDgThreads;
       int n, k;
-      if (sbk == 1) { n = e >> 5; k = e & 31; } else { k = e >> 6; n = e & 63; }
+      if (sbk == 1) { n = e >> 5; k = e & 31; } else { k = e >> 7; n = e & 127; }
       bs[k * kDgBS + n] = (double)rb[q];
     }
   };
