@@ -16,8 +16,9 @@ with x and gy copied from pinned host memory and y and dx copied back every step
 reference arm (``--impl reference``, and the ``cpu_baseline`` field) runs the UNMODIFIED reference
 package (installed by __graft_entry__.build() into the git-ignored baseline/_ref) on the box's
 host cores — or, if that install is absent, its float64 NumPy restatement in oracle/.
-Supplementary fields (not the headline): cfg2 (KAN [784,256,10] DP step), the cfg4-shaped UKAN
-layer, cfg5 (UKAN [64,512,512,64] DP training, global batch 65536 sharded), cfg1, PINN.
+Supplementary fields (not the headline): cfg2 (KAN [784,256,10] DP step), cfg4 (UKAN 1024 -> 1024
+at B = 65536, and the B = 4096 variant), cfg5 (UKAN [64,512,512,64] DP training, global batch
+65536 sharded), cfg1 (autograd API and as a captured step), PINN.
 """
 from __future__ import annotations
 
@@ -330,6 +331,7 @@ def our_arm(args, rank, world, local_rank):
         if world == 1:
             supp["cfg2_kan_stack_dp"] = cfg2_rate(dev)
             supp["ukan_layer"] = ukan_layer_rate(dev)
+            supp["cfg4_ukan_layer"] = cfg4_rate(dev)
             supp["kan_layers"] = kan_layer_rates(dev)  # cfg1 (autograd API and as a captured step)
             supp["pinn"] = pinn_rate(dev)
     if rank != 0:
@@ -499,6 +501,42 @@ def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
     n_u = P.ops.ukan_build_keys(x.detach(), 3, 0.5).n_u
     return {"workload": "UKAN layer 1024->1024 k=3 delta_g=0.5 d_pe=d_femb=32, x~N(0,20^2), B=4096 (cfg4-shaped)",
             "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "n_u": n_u, "steps": steps, "warmup": warmup}
+
+
+def cfg4_rate(dev, B=65536, steps=3, warmup=2):
+    """Supplementary cfg4 at its SURVEY 8d D4 size: one UKAN layer 1024 -> 1024, k=3, delta_g=0.5,
+    d_pe=d_femb=32, B = 65536, x ~ N(0, 20^2) with 0.1% of entries +-10^U(2,6) (criterion-10-style
+    tails), forward + backward of x and every parameter through the drop-in API, device-timed."""
+    import torch
+    import paper_2408_11200_b200 as P
+    layer = P.init_layer("ukan", 1024, 1024, 3, seed=0, delta_g=0.5, d_pe=32, d_femb=32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    x = torch.randn((B, 1024), device=dev, generator=g) * 20.0
+    m = torch.rand((B, 1024), device=dev, generator=g) < 0.001
+    tails = torch.sign(torch.randn((B, 1024), device=dev, generator=g)) * 10.0 ** (
+        2.0 + 4.0 * torch.rand((B, 1024), device=dev, generator=g))
+    x = torch.where(m, tails, x).requires_grad_(True)
+    del m, tails
+    gy = torch.randn((B, 1024), device=dev, generator=g)
+    params = [x] + list(layer.parameters().values())
+    for _ in range(warmup):
+        torch.autograd.grad(P.ukan_forward(layer, x), params, gy)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        torch.autograd.grad(P.ukan_forward(layer, x), params, gy)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    n_u = P.ops.ukan_build_keys(x.detach(), 3, 0.5).n_u
+    out = {"workload": "cfg4: UKAN layer 1024->1024 k=3 delta_g=0.5 d_pe=d_femb=32, B=65536, x~N(0,20^2) + 0.1% "
+                       "tails to 1e6, fwd + bwd of x and every parameter (drop-in API)",
+           "samples_per_s": B / (ms * 1e-3), "ms_per_step": ms, "n_u": n_u, "steps": steps, "warmup": warmup}
+    del layer, x, gy, params
+    torch.cuda.empty_cache()
+    return out
 
 
 def kan_layer_rates(dev):
