@@ -278,7 +278,8 @@ int ukan_softmax_xent(const float* logits, const int64_t* labels, double* loss,
                       double grad_scale, int32_t* err_flag, void* stream);
 
 /* Mean squared error over pred/target [n] elements (tensor.py:368-374): loss points at
- * 1 + n device doubles, loss[0] = sum (pred-target)^2 / n_global; dpred = 2*(pred-target)/n_global. */
+ * 1 + n device doubles (loss[1..] is scratch: per-256-element partial sums), loss[0] = sum (pred-target)^2
+ * / n_global; dpred = 2*(pred-target)/n_global. */
 int ukan_mse(const float* pred, const float* target, double* loss, float* dpred,
              int64_t n, int64_t n_global, void* stream);
 

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["basis.cpp", "spline.cu", "kan_fwd.cu", "kan_bwd.cu", "kan_bwd_tc.cu", "kan_bwd_sw.cu", "kan_bwd_wide.cu", "kan_fwd_tm.cu", "kan_narrow.cu", "kan_naive.cu", "kan_tangent.cu", "ukan_keys.cu", "cg.cu", "cg_tc.cu", "cg_dmma.cu", "train.cu"]
+SOURCES = ["basis.cpp", "spline.cu", "kan_fwd.cu", "kan_bwd.cu", "kan_bwd_tc.cu", "kan_bwd_sw.cu", "kan_bwd_wide.cu", "kan_fwd_tm.cu", "kan_narrow.cu", "kan_small.cu", "kan_naive.cu", "kan_tangent.cu", "ukan_keys.cu", "cg.cu", "cg_tc.cu", "cg_dmma.cu", "train.cu"]
 
 
 def _deps():

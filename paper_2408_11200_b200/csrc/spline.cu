@@ -541,6 +541,15 @@ struct TmPlan {
   int depth = 5, db = 1;
 };
 TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
+// kan_small.cu: small layers (d_in * d_out <= 2^14, k = 3, no base branch)
+bool kan_small_ok(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
+int64_t kan_small_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t G);
+int kan_small_forward(const float* x, const float* C, const float* scale, float* y, int B, int d_in, int d_out, int G,
+                      const KanGrid& grid, int32_t* err, cudaStream_t st);
+int kan_small_records(const float* x, void* ws, int B, int d_in, const KanGrid& grid, cudaStream_t st);
+int kan_small_tablegrad(const float* x, const float* C, const float* scale, const float* gy, float* dC, float* dscale,
+                        void* ws, int B, int d_in, int d_out, int G, const KanGrid& grid, bool prepared,
+                        cudaStream_t st);
 int64_t kan_fwd_tm_workspace(const TmPlan& p);
 template <int K>
 int kan_fwd_tm_run(const float* x, const float* C, const float* scale, float* y, void* ws, int64_t ws_bytes, int B,
@@ -709,6 +718,8 @@ extern "C" int ukan_kan_forward_ws(const float* x, const float* coeffs, const fl
   if (d_out <= 32 && fwd_use_tm()) {  // narrow layer: lanes over samples (kan_narrow.cu)
     UKAN_DISPATCH_K(k, return kan_fwd_narrow<K>(x, coeffs, scale, base_weight, y, (int)B, (int)d_in, (int)d_out, rm.R, rm.grid, err_flag, st););
   }
+  if (fwd_use_tm() && kan_small_ok(B, d_in, d_out, G, k, base_weight != nullptr))  // small layer
+    return kan_small_forward(x, coeffs, scale, y, (int)B, (int)d_in, (int)d_out, (int)G, rm.grid, err_flag, st);
   if (base_weight == nullptr && fwd_use_tm()) {
     const TmPlan tp = kan_fwd_tm_plan(B, d_in, d_out, G, k, false);
     if (tp.ok) {
@@ -737,6 +748,7 @@ extern "C" int ukan_kan_forward(const float* x, const float* coeffs, const float
 extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int64_t d_out,
                                                     int64_t G, int k) {
   if (k < 0 || k > UKAN_MAX_DEGREE || G < 1 || B < 0 || d_in < 1 || d_out < 1) return 0;
+  const int64_t sm = kan_small_ok(B, d_in, d_out, G, k, false) ? kan_small_workspace(B, d_in, d_out, G) : 0;
   RegPlan dp;
   const bool dm = kan_bwd_dmma_plan(B, d_in, d_out, (int)(G + k), k + 1, false, kan_num_sms(), dp);
   const RegPlan p = kan_bwd_reg_plan(B, d_in, d_out, (int)(G + k), k + 1, true, kan_num_sms());
@@ -744,10 +756,11 @@ extern "C" int64_t ukan_kan_backward_workspace_size(int64_t B, int64_t d_in, int
   const int64_t sw = kan_bwd_sw_workspace(kan_bwd_sw_plan(B, d_in, d_out, (int)(G + k), k + 1, true));
   const int64_t wd = kan_bwd_wide_workspace(kan_bwd_wide_plan(B, d_in, d_out, (int)(G + k), k + 1));
   static const bool force_wide = getenv("UKAN_BWD") && getenv("UKAN_BWD")[0] == 'w';
-  if ((!p.ok || force_wide) && wd > 0) return std::max<int64_t>(wd, p.ok ? p.ws_bytes : 0);
-  if (p.ok) return std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc), sw);
-  if (bwd_fits_smem(k + 1, (int)(G + k))) return 0;
-  return (int64_t)sizeof(double) * d_in * (G + k) * d_out;
+  if ((!p.ok || force_wide) && wd > 0) return std::max<int64_t>(std::max<int64_t>(wd, p.ok ? p.ws_bytes : 0), sm);
+  if (p.ok)
+    return std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(p.ws_bytes, dm ? dp.ws_bytes : 0), tc), sw), sm);
+  if (bwd_fits_smem(k + 1, (int)(G + k))) return sm;
+  return std::max<int64_t>((int64_t)sizeof(double) * d_in * (G + k) * d_out, sm);
 }
 
 // A side stream per (host thread, device) to overlap two independent small kernels of one call:
@@ -799,6 +812,21 @@ static int kan_backward_impl(const float* x, const float* coeffs, const float* s
   if (table_done) {
     if (dx) {
       if (d_out <= 32) return kan_dx_narrow2<K>(x, coeffs, scale, bw, gy, dx, B, d_in, d_out, rm.R, rm.grid, st);
+      const Basis<K> bas = make_basis<K>(K - 1);
+      const int64_t pairs = (int64_t)B * d_in;
+      spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
+                                                                             d_out, rm, bas);
+      UKAN_LAUNCH_CHECK();
+    }
+    return UKAN_OK;
+  }
+  if (sel[0] == 't' && K == 4 && bw == nullptr && B > 0 && kan_small_ok(B, d_in, d_out, rm.R - K + 1, K - 1, false) &&
+      workspace != nullptr && workspace_bytes >= kan_small_workspace(B, d_in, d_out, rm.R - K + 1)) {
+    // small layer (kan_small.cu): table gradient over >= 256 CTAs, dx by the per-pair kernel
+    int rc = kan_small_tablegrad(x, coeffs, scale, gy, dC, dscale, workspace, B, d_in, d_out, rm.R - K + 1, rm.grid,
+                                 prepared, st);
+    if (rc) return rc;
+    if (dx) {
       const Basis<K> bas = make_basis<K>(K - 1);
       const int64_t pairs = (int64_t)B * d_in;
       spline_dx_kernel<K, false><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, coeffs, scale, bw, gy, dx, B, d_in,
@@ -910,7 +938,7 @@ extern "C" int ukan_kan_backward_ws2(const float* x, const float* coeffs, const 
 
 extern "C" int ukan_kan_backward_part_supported(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k) {
   if (check_kan_args(B, d_in, d_out, G, k, -1.0, 1.0) || B < 1) return 0;
-  if (kan_bwd_selector()[0] != 't') return 0;
+  if (kan_bwd_selector()[0] != 't' || kan_small_ok(B, d_in, d_out, G, k, false)) return 0;
   const TcPlan p = kan_bwd_tc_plan(B, d_in, d_out, G, k, false);
   return (p.ok && d_out >= 64 && d_out % 4 == 0) ? 1 : 0;
 }
@@ -947,6 +975,12 @@ extern "C" int ukan_kan_backward_prep(const float* x, const float* base_weight, 
   if (rc) return rc;
   const char* sel = kan_bwd_selector();
   if (B < 1 || k != 3 || base_weight != nullptr || sel[0] != 't' || x == nullptr) return UKAN_OK;
+  if (kan_small_ok(B, d_in, d_out, G, k, false)) {  // small layer: the records of kan_small.cu
+    if (workspace == nullptr || workspace_bytes < kan_small_workspace(B, d_in, d_out, G)) return UKAN_OK;
+    rc = kan_small_records(x, workspace, (int)B, (int)d_in, make_kan_grid(g_min, g_max, G), (cudaStream_t)stream);
+    if (rc == UKAN_OK) *prepared = 1;
+    return rc;
+  }
   const TcPlan tp = kan_bwd_tc_plan(B, d_in, d_out, G, k, false);
   if (!tp.ok || workspace == nullptr || workspace_bytes < kan_bwd_tc_workspace(tp)) return UKAN_OK;
   rc = kan_bwd_tc_prep(x, workspace, workspace_bytes, (int)B, (int)d_in, (int)G, make_kan_grid(g_min, g_max, G), tp,

@@ -37,14 +37,25 @@ __global__ void xent_rows_kernel(const float* __restrict__ logits, const int64_t
   }
 }
 
-__global__ void mse_rows_kernel(const float* __restrict__ pred, const float* __restrict__ target,
-                                double* __restrict__ sq, float* __restrict__ dpred, int64_t n,
-                                double two_over_n) {
+// Squared errors summed per 256-element block in a fixed tree order (deterministic), so the final
+// single-CTA sum reads n / 256 partials instead of n.
+__global__ void __launch_bounds__(256) mse_rows_kernel(const float* __restrict__ pred, const float* __restrict__ target,
+                                                       double* __restrict__ sq, float* __restrict__ dpred, int64_t n,
+                                                       double two_over_n) {
+  __shared__ double sm[256];
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const double d = (double)pred[t] - (double)target[t];
-  sq[t] = d * d;
-  dpred[t] = (float)(two_over_n * d);
+  double d = 0.0;
+  if (t < n) {
+    d = (double)pred[t] - (double)target[t];
+    dpred[t] = (float)(two_over_n * d);
+  }
+  sm[threadIdx.x] = d * d;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sq[blockIdx.x] = sm[0];
 }
 
 // Deterministic single-CTA sum of v[0..n) scaled by `scale` into *out.
@@ -147,7 +158,7 @@ extern "C" int ukan_mse(const float* pred, const float* target, double* loss, fl
   double* rows = loss + 1;  // caller provides loss[1 + n] doubles
   mse_rows_kernel<<<nblk(n, 256), 256, 0, st>>>(pred, target, rows, dpred, n, 2.0 / (double)n_global);
   UKAN_LAUNCH_CHECK();
-  sum_f64_kernel<<<1, 1024, 0, st>>>(rows, n, 1.0 / (double)n_global, loss);
+  sum_f64_kernel<<<1, 1024, 0, st>>>(rows, nblk(n, 256), 1.0 / (double)n_global, loss);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }

@@ -90,10 +90,10 @@ def test_two_ranks_uneven_shards_match_single_process(kind):
     np.testing.assert_array_equal(res[0][2], res[1][2])
 
 
-def _layer_run(x, gy, world=1, rank=0, buckets=3):
+def _layer_run(x, gy, world=1, rank=0, buckets=3, d_out=64):
     import paper_2408_11200_b200 as P
     from paper_2408_11200_b200.train import shard_bounds
-    layer = P.init_layer("kan", 24, 64, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
+    layer = P.init_layer("kan", 24, d_out, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
     tr = P.LayerTrainer(layer, 1e-2, buckets=buckets)
     lo, hi = shard_bounds(x.shape[0], rank, world)
     y, dx = tr.step(torch.tensor(x[lo:hi], device="cuda"), torch.tensor(gy[lo:hi], device="cuda"))
@@ -101,32 +101,40 @@ def _layer_run(x, gy, world=1, rank=0, buckets=3):
     return (y.cpu().numpy(), dx.cpu().numpy(), tr.flat.grad.cpu().numpy().copy(), tr.flat.data.cpu().numpy().copy())
 
 
-def _layer_data():
+def _layer_data(d_out=64):
     rng = np.random.default_rng(8)
     x = rng.uniform(-1.2, 1.2, (301, 24)).astype(np.float32)
-    gy = (rng.normal(size=(301, 64)) / 301).astype(np.float32)  # dL/dy of a global mean loss
+    gy = (rng.normal(size=(301, d_out)) / 301).astype(np.float32)  # dL/dy of a global mean loss
     return x, gy
 
 
-def _layer_worker(rank, world, port, q):
+def _layer_worker(rank, world, port, q, d_out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        x, gy = _layer_data()
-        q.put((rank, _layer_run(x, gy, world, rank)))
+        x, gy = _layer_data(d_out)
+        q.put((rank, _layer_run(x, gy, world, rank, d_out=d_out)))
     finally:
         dist.destroy_process_group()
 
 
-def test_layer_trainer_matches_autograd_and_oracle():
+# d_out 704: the bucketed ukan_kan_backward_part path; d_out 64 (d_in * d_out <= 2^14): the small-
+# layer path (kan_small.cu) through ukan_kan_backward_ws2 and one all-reduce of the whole gradient.
+LAYER_D_OUT = [704, 64]
+
+
+@pytest.mark.parametrize("d_out", LAYER_D_OUT)
+def test_layer_trainer_matches_autograd_and_oracle(d_out):
     """LayerTrainer (the bench's cfg3 unit: dx first, then the table gradient in feature buckets
-    via ukan_kan_backward_part) against the drop-in autograd path and the oracle."""
+    via ukan_kan_backward_part) against the oracle; bucketing changes no bit."""
     import oracle
     import paper_2408_11200_b200 as P
-    x, gy = _layer_data()
-    y, dx, grad, _ = _layer_run(x, gy, buckets=3)
-    layer = P.init_layer("kan", 24, 64, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
+    from paper_2408_11200_b200 import _lib
+    assert _lib.load().ukan_kan_backward_part_supported(301, 24, d_out, 16, 3) == (1 if d_out == 704 else 0)
+    x, gy = _layer_data(d_out)
+    y, dx, grad, _ = _layer_run(x, gy, buckets=3, d_out=d_out)
+    layer = P.init_layer("kan", 24, d_out, 3, seed=3, g_min=-1.0, g_max=1.0, G=16, device="cuda")
     p = {n: t.detach().double().cpu().numpy() for n, t in layer.parameters().items()}
     want = oracle.kan_forward_backward(x.astype(np.float64), p["coeffs"], p["scale"], gy.astype(np.float64), k=3,
                                        g_min=-1.0, g_max=1.0, G=16)
@@ -135,23 +143,24 @@ def test_layer_trainer_matches_autograd_and_oracle():
     nC = p["coeffs"].size
     assert_close(grad[:nC].reshape(p["coeffs"].shape), want["dcoeffs"], what="dcoeffs")
     assert_close(grad[nC:].reshape(p["scale"].shape), want["dscale"], what="dscale")
-    _, _, grad1, _ = _layer_run(x, gy, buckets=1)
+    _, _, grad1, _ = _layer_run(x, gy, buckets=1, d_out=d_out)
     np.testing.assert_array_equal(grad, grad1)  # bucketing does not change a bit
 
 
-def test_layer_trainer_two_ranks_match_single_process():
+@pytest.mark.parametrize("d_out", LAYER_D_OUT)
+def test_layer_trainer_two_ranks_match_single_process(d_out):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_layer_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_layer_worker, args=(r, 2, port, q, d_out)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(2))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    x, gy = _layer_data()
-    y1, dx1, grad1, data1 = _layer_run(x, gy)
+    x, gy = _layer_data(d_out)
+    y1, dx1, grad1, data1 = _layer_run(x, gy, d_out=d_out)
     from paper_2408_11200_b200.train import shard_bounds
     for r in (0, 1):
         lo, hi = shard_bounds(x.shape[0], r, 2)

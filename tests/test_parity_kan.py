@@ -201,3 +201,35 @@ def test_tmem_forward_fine_grid_variants(G):
     """TMEM-gather forward around its plan boundaries: G=37 (5-deep ring, two TMEM slabs), G=48
     (3-deep ring, one slab) and G=64 (one slab of 67 x 4 columns); d_out >= 128 takes that path."""
     check_against_oracle(*random_case(300, 5, 130, 3, G, seed=60 + G, outliers=0.05), need_dx=False)
+
+
+@pytest.mark.parametrize("B,d_in,d_out,G,outliers", [(1, 1, 33, 3, 0.0), (37, 5, 100, 10, 0.2), (1024, 64, 64, 10, 0.05),
+                                                     (1500, 16, 200, 40, 0.1), (6000, 16, 64, 10, 0.0),
+                                                     (300, 2, 4096, 97, 0.0)])
+def test_small_layer_path(B, d_in, d_out, G, outliers):
+    """kan_small.cu (d_in * d_out <= 2^14, B * d_in * d_out <= 6 Mi, k = 3, no base): ragged output
+    tiles (d_out not a multiple of 64), one sample, one feature, 375 samples per thread, the
+    largest grid (R = 100 rows: 4 sample splits), outliers."""
+    layer, x, gup = random_case(B, d_in, d_out, 3, G, seed=B + d_in, outliers=outliers)
+    check_against_oracle(layer, x, gup)
+
+
+def test_small_layer_prepared_records_and_determinism():
+    """SplineTrainer builds the first layer's records on a side stream (ukan_kan_backward_prep ->
+    kan_small_records); the step must equal the eager autograd step bitwise, twice."""
+    x = np.random.default_rng(3).uniform(-1, 1, (1024, 64)).astype(np.float32)
+    t = np.random.default_rng(4).normal(size=(1024, 64)).astype(np.float32)
+    grads = []
+    for _ in range(2):
+        model = P.build_model("kan", [64, 64], 3, seed=0, device=DEV, g_min=-1.0, g_max=1.0, G=10)
+        tr = P.SplineTrainer(model, "mse", 1e-3, "adam")
+        tr.read_loss(tr.step(torch.tensor(x, device=DEV), torch.tensor(t, device=DEV)))
+        grads.append(tr.flat.grad.cpu().numpy().copy())
+    np.testing.assert_array_equal(grads[0], grads[1])
+    layer = P.init_layer("kan", 64, 64, 3, seed=0, g_min=-1.0, g_max=1.0, G=10)
+    p = {n: v.detach().double().cpu().numpy() for n, v in layer.parameters().items()}
+    cfg = dict(k=3, g_min=-1.0, g_max=1.0, G=10)
+    _, want, _, _, _ = oracle.model_step("kan", [p], [cfg], x.astype(np.float64), t.astype(np.float64), "mse", 1e-3)
+    nC = p["coeffs"].size
+    assert_close(grads[0][:nC].reshape(p["coeffs"].shape), want[0]["coeffs"], what="dcoeffs")
+    assert_close(grads[0][nC:].reshape(p["scale"].shape), want[0]["scale"], what="dscale")
