@@ -21,6 +21,9 @@
 //    each row is the sum of the two blocks holding it, reduced in fixed order at the end.
 // Deterministic: fixed sample order per chunk, fixed chunk order, fixed reductions.  IEEE fp64
 // products and sums throughout.
+#include <cuda.h>  // CUtensorMap (the 2-D TMA descriptor of the tc3 sweep)
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -491,6 +494,235 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// "tc3": the tc2 sweep (NT = 4) fed by TMA and synchronised by mbarriers instead of CTA barriers.
+//  * one elected thread streams each chunk into a 2-deep shared ring: the g tile [256 samples x
+//    32 outputs] with ONE 2-D tensor-map TMA (cp.async.bulk.tensor, 128-byte swizzle, zero fill
+//    beyond B / d_out) and the FPB feature records with 1-D bulk copies, all completing on the
+//    stage's `full` mbarrier — in place of ~2,900 cp.async issued by every thread per chunk;
+//  * each warp evaluates the fp64 basis weights of exactly the sorted positions of its own blocks
+//    (its samples are a contiguous run of the cell-sorted chunk) into the stage's weight buffer,
+//    so no CTA-wide barrier separates the weight phase from the DMMA phase;
+//  * a warp releases a stage with one arrive on its `empty` mbarrier; the next-but-one chunk is
+//    loaded into a stage once every warp has released it, so warps drift up to one chunk apart
+//    (which also keeps the two weight buffers race-free: the block -> position map changes per
+//    chunk, so a warp one chunk ahead writes positions another warp may still be reading).
+// Same group order and weight formula as tc2: bitwise-identical results.
+static __device__ __forceinline__ void tc_mb_init(uint64_t* mb, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(count));
+}
+static __device__ __forceinline__ void tc_mb_expect_tx(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)),
+               "r"(bytes)
+               : "memory");
+}
+static __device__ __forceinline__ void tc_mb_arrive(uint64_t* mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)) : "memory");
+}
+static __device__ __forceinline__ void tc_mb_wait(uint64_t* mb, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mb);
+  asm volatile(
+      "{\n.reg .pred p;\nTCW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TCW_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+static __device__ __forceinline__ void tc_bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(mb))
+               : "memory");
+}
+static __device__ __forceinline__ void tc_tma_2d(void* smem, const CUtensorMap* map, int c0, int c1, uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"((uint32_t)__cvta_generic_to_shared(mb))
+      : "memory");
+}
+
+constexpr int kTc3Depth = 2;
+constexpr uint32_t kTc3GBytes = kTcBC * 32 * 4;  // one g tile: 256 samples x 32 outputs fp32
+
+template <int RB, int FPB, int WPF>
+__global__ void __launch_bounds__(FPB * WPF * 32, 1)
+kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigned char* __restrict__ recs,
+                         const float* __restrict__ C, const float* __restrict__ scale, float* __restrict__ dC,
+                         float* __restrict__ dscale, double* __restrict__ part, int B, int d_in, int d_out, int G,
+                         int nch, int cps, Basis<4> bas) {
+  constexpr int NT = 4, OPB = 32;
+  constexpr int BH = RB / WPF;
+  constexpr int NWARP = FPB * WPF;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_s[kTc3Depth], empty_s[kTc3Depth];
+  __shared__ double Msh[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, kq = lane & 3;
+  const int fl = warp / WPF, h = warp % WPF;
+  constexpr int kSwFG = 16;  // grid walk in panels of feature groups (as tc2)
+  int ot, fg;
+  {
+    const int n_ot = gridDim.x, n_fg = gridDim.y;
+    const int L = blockIdx.y * n_ot + blockIdx.x;
+    const int pw = min(kSwFG, n_fg);
+    const int sc = L / (pw * n_ot), r = L % (pw * n_ot);
+    const int pe = min(pw, n_fg - sc * pw);
+    ot = r / pe;
+    fg = sc * pw + r % pe;
+  }
+  const int i0 = fg * FPB;
+  const int i = i0 + fl;
+  const int o0 = ot * OPB;
+  const int z = blockIdx.z;
+  const int n_lo = z * cps, n_hi = min(nch, n_lo + cps);
+  const int R = G + 3;
+  const size_t rb = tc_rec_bytes(G);
+  const int nf = min(FPB, d_in - i0);  // features of this CTA with records
+  // smem: g ring (1024-aligned for the 128-byte swizzle) | record ring | weight ring
+  unsigned char* g_ring =  // the 128-byte swizzle needs 1024-byte aligned tiles
+      smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  unsigned char* rec_ring = g_ring + kTc3Depth * kTc3GBytes;
+  double* w_ring = reinterpret_cast<double*>(rec_ring + (size_t)kTc3Depth * FPB * rb);  // [depth][FPB][BC][4]
+  const bool producer = threadIdx.x == 0;
+  if (producer) {
+    for (int d = 0; d < kTc3Depth; ++d) {
+      tc_mb_init(&full_s[d], 1);
+      tc_mb_init(&empty_s[d], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Msh[q] = bas.M[q / 4][q % 4];
+  }
+  __syncthreads();
+  auto issue = [&](int c) {  // chunk n_lo + c -> stage c % depth
+    const int n = n_lo + c, d = c % kTc3Depth;
+    uint64_t* mb = &full_s[d];
+    tc_mb_expect_tx(mb, kTc3GBytes + (uint32_t)(nf * rb));
+    tc_tma_2d(g_ring + (size_t)d * kTc3GBytes, &gmap, o0, n * kTcBC, mb);
+    for (int f = 0; f < nf; ++f)
+      tc_bulk_g2s(rec_ring + ((size_t)d * FPB + f) * rb, recs + ((size_t)(i0 + f) * nch + n) * rb, (uint32_t)rb, mb);
+  };
+  const int nchunk = n_hi - n_lo;
+  if (producer)
+    for (int c = 0; c < min(kTc3Depth, nchunk); ++c) issue(c);
+
+  double acc[BH][NT][2];
+#pragma unroll
+  for (int bb = 0; bb < BH; ++bb)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[bb][t][0] = acc[bb][t][1] = 0.0;
+  for (int c = 0; c < nchunk; ++c) {
+    const int d = c % kTc3Depth;
+    double* wf = w_ring + ((size_t)d * FPB + fl) * kTcBC * 4;
+    tc_mb_wait(&full_s[d], (uint32_t)((c / kTc3Depth) & 1));
+    if (i < d_in) {
+      const unsigned char* rec = rec_ring + ((size_t)d * FPB + fl) * rb;
+      const int* ent = reinterpret_cast<const int*>(rec);
+      const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
+      const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
+      // this warp's sorted positions: the cells of its blocks [h*BH, (h+1)*BH)
+      const int p_lo = st[min(4 * h * BH, G)], p_hi = st[min(4 * (h + 1) * BH, G)];
+      for (int p = p_lo + lane; p < p_hi; p += 32) {  // fp64 Horner, layers.py:29-37
+        const double u = uu[p];
+        double* wd = wf + (size_t)p * 4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wd[j] = fma(fma(fma(Msh[12 + j], u, Msh[8 + j]), u, Msh[4 + j]), u, Msh[j]);
+      }
+      __syncwarp();
+      const unsigned char* gt = g_ring + (size_t)d * kTc3GBytes;
+      // B operand: lane (sample kq, column grp) of tile t is output o0 + grp*NT + t: the 16-byte
+      // chunk grp of the sample's 128-byte row, stored at chunk grp ^ (row & 7) (128-byte swizzle)
+      auto load_group = [&](int kc, int e1, double& a, float4& gv) {
+        const int pos = kc + kq;
+        const int pc = pos < e1 ? pos : kc;  // masked lanes read an own, finished position
+        const int e = ent[pc];
+        const int j = grp - ((e >> 8) & 3);
+        const double wj = wf[pc * 4 + (j & 3)];
+        a = (pos < e1 && j >= 0 && j < 4) ? wj : 0.0;
+        const int srow = e & 255;
+        gv = *reinterpret_cast<const float4*>(gt + srow * 128 + ((grp ^ (srow & 7)) << 4));
+      };
+#pragma unroll
+      for (int bl = 0; bl < BH; ++bl) {
+        const int bb = h * BH + bl;
+        const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
+        int kc = e0;
+        for (; kc + 4 < e1; kc += 8) {  // two groups in flight
+          double a0, a1;
+          float4 g0, g1;
+          load_group(kc, e1, a0, g0);
+          load_group(kc + 4, e1, a1, g1);
+          tc_dmma(acc[bl][0][0], acc[bl][0][1], a0, (double)g0.x);
+          tc_dmma(acc[bl][1][0], acc[bl][1][1], a0, (double)g0.y);
+          tc_dmma(acc[bl][2][0], acc[bl][2][1], a0, (double)g0.z);
+          tc_dmma(acc[bl][3][0], acc[bl][3][1], a0, (double)g0.w);
+          tc_dmma(acc[bl][0][0], acc[bl][0][1], a1, (double)g1.x);
+          tc_dmma(acc[bl][1][0], acc[bl][1][1], a1, (double)g1.y);
+          tc_dmma(acc[bl][2][0], acc[bl][2][1], a1, (double)g1.z);
+          tc_dmma(acc[bl][3][0], acc[bl][3][1], a1, (double)g1.w);
+        }
+        if (kc < e1) {
+          double a0;
+          float4 g0;
+          load_group(kc, e1, a0, g0);
+          tc_dmma(acc[bl][0][0], acc[bl][0][1], a0, (double)g0.x);
+          tc_dmma(acc[bl][1][0], acc[bl][1][1], a0, (double)g0.y);
+          tc_dmma(acc[bl][2][0], acc[bl][2][1], a0, (double)g0.z);
+          tc_dmma(acc[bl][3][0], acc[bl][3][1], a0, (double)g0.w);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc_mb_arrive(&empty_s[d]);
+    // refill this stage with chunk c+2 once every warp has released chunk c
+    if (producer && c + kTc3Depth < nchunk) {
+      tc_mb_wait(&empty_s[d], (uint32_t)((c / kTc3Depth) & 1));
+      issue(c + kTc3Depth);
+    }
+  }
+  __syncthreads();  // every stage consumed (all issued loads were waited on): the ring is free
+  // epilogue (as tc2): rows of both halves meet in S[FPB][R][OPB] (fp64, reuses the ring)
+  double* S = reinterpret_cast<double*>(g_ring);
+  const int RR = 4 * RB + 4;
+  for (int t = threadIdx.x; t < FPB * RR * OPB; t += blockDim.x) S[t] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int hh = 0; hh < WPF; ++hh) {
+    if (h == hh) {
+#pragma unroll
+      for (int bl = 0; bl < BH; ++bl) {
+        const int r = 4 * (h * BH + bl) + grp;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) S[((size_t)fl * RR + r) * OPB + (2 * kq + v) * NT + t] += acc[bl][t][v];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < FPB * OPB; t += blockDim.x) {
+    const int f = t / OPB, oc = t % OPB;
+    const int ii = i0 + f, o = o0 + oc;
+    if (ii >= d_in || o >= d_out) continue;
+    const double* Sf = S + (size_t)f * RR * OPB + oc;
+    if (part != nullptr) {
+      for (int r = 0; r < R; ++r) part[(size_t)z * d_in * R * d_out + ((size_t)ii * R + r) * d_out + o] = Sf[(size_t)r * OPB];
+    } else {
+      const double sc = (double)scale[(size_t)ii * d_out + o];
+      double ds = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const size_t ci = ((size_t)ii * R + r) * d_out + o;
+        const double a = Sf[(size_t)r * OPB];
+        dC[ci] = (float)(sc * a);
+        ds = fma((double)C[ci], a, ds);
+      }
+      dscale[(size_t)ii * d_out + o] = (float)ds;
+    }
+  }
+}
+
 // Fixed-order reduction of the split-batch partials + epilogue: CTA = (feature i, 32 outputs);
 // threads sweep the (row, output) pairs (coalesced over o): dC = scale * sum_z part, and the
 // per-row products C * A meet in shared memory for dscale = sum_r C * A (row order).
@@ -624,6 +856,57 @@ static int tc2_launch(const float* C, const float* scale, const float* gy, float
   return UKAN_OK;
 }
 
+// 2-D tensor map of g [B, d_out] fp32: box 32 outputs x 256 samples, 128-byte swizzle, zero fill
+static bool tc3_tensor_map(CUtensorMap* map, const float* gy, int B, int d_out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (encode == nullptr) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)d_out, (cuuint64_t)B};
+  const cuuint64_t strides[1] = {(cuuint64_t)d_out * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)kTcBC};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gy), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static size_t tc3_smem(int G, int fpb, int rb16) {
+  const size_t ring = (size_t)kTc3Depth * kTc3GBytes + (size_t)kTc3Depth * fpb * tc_rec_bytes(G) +
+                      sizeof(double) * (size_t)kTc3Depth * fpb * kTcBC * 4;
+  return 1024 + std::max(ring, sizeof(double) * (size_t)fpb * (4 * rb16 + 4) * 32);  // + alignment slack
+}
+
+// tc3 applies to the NT = 4 tc2 shapes (32-output tiles) with 16-byte aligned g rows
+static bool tc3_enabled() {
+  static const bool off = getenv("UKAN_TC3") && getenv("UKAN_TC3")[0] == '0';  // A/B measurement only
+  return !off;
+}
+
+template <int RB, int FPB, int WPF>
+static int tc3_launch(const CUtensorMap& map, const float* C, const float* scale, float* dC, float* dscale,
+                      unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
+                      cudaStream_t st) {
+  auto kern = kan_bwd_tc3_sweep_kernel<RB, FPB, WPF>;
+  const size_t smem = tc3_smem(G, FPB, RB);
+  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 gridd((d_out + 31) / 32, (d_in + FPB - 1) / FPB, p.S);
+  kern<<<gridd, FPB * WPF * 32, smem, st>>>(map, recs, C, scale, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
+                                            p.nch, p.cps, make_basis<4>(3));
+  UKAN_LAUNCH_CHECK();
+  if (p.S > 1) {
+    kan_bwd_tc_reduce_kernel<<<dim3(d_in, (d_out + 31) / 32), 256, sizeof(double) * (G + 3) * 32, st>>>(
+        part, C, scale, dC, dscale, p.S, d_in, d_out, G + 3);
+    UKAN_LAUNCH_CHECK();
+  }
+  return UKAN_OK;
+}
+
 template <int RB, int NT>
 static int tc_launch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                      unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
@@ -660,6 +943,10 @@ static int tc_sweep_dispatch(const float* C, const float* scale, const float* gy
   if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  CUtensorMap map;  // tc3: the driver's tensor-map encoder is required (else the tc2 sweep runs)
+  if (tc3_enabled() && (d_out % 4) == 0 && ((uintptr_t)gy % 16) == 0 && p.split && p.rb == 16 && p.wpf == 4 &&
+      p.nt == 4 && tc3_tensor_map(&map, gy, B, d_out))
+    return tc3_launch<16, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 4) return tc2_launch<16, 4, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8 && p.fpb == 2) return tc2_launch<16, 8, 2, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8) return tc2_launch<16, 4, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
