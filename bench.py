@@ -344,7 +344,7 @@ def our_arm(args, rank, world, local_rank):
         "forward": ("kan_fwd_tm_kernel (TMEM gather, FP32 FMA; + pack / records pre-passes)", FP32_TFLOPS_MEASURED,
                     "fp32 FMA (tools/peaks.cu)"),
         "backward_dx": ("kan_dx_tc_kernel (dx on FP64 DMMA)", DMMA_TFLOPS_MEASURED, "FP64 DMMA (tools/dmma_peak.cu)"),
-        "backward_table": ("kan_bwd_tc2_sweep_kernel<16,4,4,4> x 8 feature buckets (dC/dscale on FP64 DMMA)",
+        "backward_table": ("kan_bwd_tc3_sweep_kernel<16,4,4,4> x 8 feature buckets (dC/dscale on FP64 DMMA, TMA-fed)",
                            DMMA_TFLOPS_MEASURED, "FP64 DMMA (tools/dmma_peak.cu)"),
     }
     dom = max((p for p in phase_info if p in phase_ms), key=lambda p: phase_ms[p])

@@ -495,10 +495,11 @@ kan_bwd_tc2_sweep_kernel(const unsigned char* __restrict__ recs, const float* __
 }
 
 // ---------------------------------------------------------------------------------------
-// "tc3": the tc2 sweep (NT = 4) fed by TMA and synchronised by mbarriers instead of CTA barriers.
+// "tc3": the tc2 sweep (NT = 4 or 8, 4 warps per feature) fed by TMA and synchronised by mbarriers
+// instead of CTA barriers.
 //  * one elected thread streams each chunk into a 2-deep shared ring: the g tile [256 samples x
-//    32 outputs] with ONE 2-D tensor-map TMA (cp.async.bulk.tensor, 128-byte swizzle, zero fill
-//    beyond B / d_out) and the FPB feature records with 1-D bulk copies, all completing on the
+//    8*NT outputs] with one 2-D tensor-map TMA per 32 outputs (cp.async.bulk.tensor, 128-byte
+//    swizzle, zero fill beyond B / d_out) and the FPB feature records with 1-D bulk copies, all completing on the
 //    stage's `full` mbarrier — in place of ~2,900 cp.async issued by every thread per chunk;
 //  * each warp evaluates the fp64 basis weights of exactly the sorted positions of its own blocks
 //    (its samples are a contiguous run of the cell-sorted chunk) into the stage's weight buffer,
@@ -543,15 +544,17 @@ static __device__ __forceinline__ void tc_tma_2d(void* smem, const CUtensorMap* 
 }
 
 constexpr int kTc3Depth = 2;
-constexpr uint32_t kTc3GBytes = kTcBC * 32 * 4;  // one g tile: 256 samples x 32 outputs fp32
+constexpr uint32_t kTc3BoxBytes = kTcBC * 32 * 4;  // one TMA box: 256 samples x 32 outputs fp32
 
-template <int RB, int FPB, int WPF>
+template <int RB, int NT, int FPB, int WPF>
 __global__ void __launch_bounds__(FPB * WPF * 32, 1)
 kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigned char* __restrict__ recs,
                          const float* __restrict__ C, const float* __restrict__ scale, float* __restrict__ dC,
                          float* __restrict__ dscale, double* __restrict__ part, int B, int d_in, int d_out, int G,
                          int nch, int cps, Basis<4> bas) {
-  constexpr int NT = 4, OPB = 32;
+  constexpr int OPB = 8 * NT, NBOX = OPB / 32;
+  constexpr uint32_t kTc3GBytes = NBOX * kTc3BoxBytes;  // one g stage: 256 samples x OPB outputs
+  static_assert(NT == 4 || NT == 8, "32-output TMA boxes");
   constexpr int BH = RB / WPF;
   constexpr int NWARP = FPB * WPF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -599,7 +602,9 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
     const int n = n_lo + c, d = c % kTc3Depth;
     uint64_t* mb = &full_s[d];
     tc_mb_expect_tx(mb, kTc3GBytes + (uint32_t)(nf * rb));
-    tc_tma_2d(g_ring + (size_t)d * kTc3GBytes, &gmap, o0, n * kTcBC, mb);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      tc_tma_2d(g_ring + (size_t)d * kTc3GBytes + bx * kTc3BoxBytes, &gmap, o0 + 32 * bx, n * kTcBC, mb);
     for (int f = 0; f < nf; ++f)
       tc_bulk_g2s(rec_ring + ((size_t)d * FPB + f) * rb, recs + ((size_t)(i0 + f) * nch + n) * rb, (uint32_t)rb, mb);
   };
@@ -631,9 +636,9 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
       }
       __syncwarp();
       const unsigned char* gt = g_ring + (size_t)d * kTc3GBytes;
-      // B operand: lane (sample kq, column grp) of tile t is output o0 + grp*NT + t: the 16-byte
-      // chunk grp of the sample's 128-byte row, stored at chunk grp ^ (row & 7) (128-byte swizzle)
-      auto load_group = [&](int kc, int e1, double& a, float4& gv) {
+      // B operand: lane (sample kq, column grp) of tile t is output o0 + grp*NT + t: 16-byte chunks
+      // grp*NT/4 + q of the sample's row, chunk c of a box row stored at c ^ (row & 7) (128-byte swizzle)
+      auto load_group = [&](int kc, int e1, double& a, float4 (&gv)[NT / 4]) {
         const int pos = kc + kq;
         const int pc = pos < e1 ? pos : kc;  // masked lanes read an own, finished position
         const int e = ent[pc];
@@ -641,7 +646,11 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
         const double wj = wf[pc * 4 + (j & 3)];
         a = (pos < e1 && j >= 0 && j < 4) ? wj : 0.0;
         const int srow = e & 255;
-        gv = *reinterpret_cast<const float4*>(gt + srow * 128 + ((grp ^ (srow & 7)) << 4));
+#pragma unroll
+        for (int q = 0; q < NT / 4; ++q) {
+          const int cc = grp * (NT / 4) + q;
+          gv[q] = *reinterpret_cast<const float4*>(gt + (cc >> 3) * kTc3BoxBytes + srow * 128 + (((cc & 7) ^ (srow & 7)) << 4));
+        }
       };
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
@@ -650,26 +659,29 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
         int kc = e0;
         for (; kc + 4 < e1; kc += 8) {  // two groups in flight
           double a0, a1;
-          float4 g0, g1;
+          float4 g0[NT / 4], g1[NT / 4];
           load_group(kc, e1, a0, g0);
           load_group(kc + 4, e1, a1, g1);
-          tc_dmma(acc[bl][0][0], acc[bl][0][1], a0, (double)g0.x);
-          tc_dmma(acc[bl][1][0], acc[bl][1][1], a0, (double)g0.y);
-          tc_dmma(acc[bl][2][0], acc[bl][2][1], a0, (double)g0.z);
-          tc_dmma(acc[bl][3][0], acc[bl][3][1], a0, (double)g0.w);
-          tc_dmma(acc[bl][0][0], acc[bl][0][1], a1, (double)g1.x);
-          tc_dmma(acc[bl][1][0], acc[bl][1][1], a1, (double)g1.y);
-          tc_dmma(acc[bl][2][0], acc[bl][2][1], a1, (double)g1.z);
-          tc_dmma(acc[bl][3][0], acc[bl][3][1], a1, (double)g1.w);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float v0 = t % 4 == 0 ? g0[t / 4].x : t % 4 == 1 ? g0[t / 4].y : t % 4 == 2 ? g0[t / 4].z : g0[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a0, (double)v0);
+          }
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float v1 = t % 4 == 0 ? g1[t / 4].x : t % 4 == 1 ? g1[t / 4].y : t % 4 == 2 ? g1[t / 4].z : g1[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a1, (double)v1);
+          }
         }
         if (kc < e1) {
           double a0;
-          float4 g0;
+          float4 g0[NT / 4];
           load_group(kc, e1, a0, g0);
-          tc_dmma(acc[bl][0][0], acc[bl][0][1], a0, (double)g0.x);
-          tc_dmma(acc[bl][1][0], acc[bl][1][1], a0, (double)g0.y);
-          tc_dmma(acc[bl][2][0], acc[bl][2][1], a0, (double)g0.z);
-          tc_dmma(acc[bl][3][0], acc[bl][3][1], a0, (double)g0.w);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float v0 = t % 4 == 0 ? g0[t / 4].x : t % 4 == 1 ? g0[t / 4].y : t % 4 == 2 ? g0[t / 4].z : g0[t / 4].w;
+            tc_dmma(acc[bl][t][0], acc[bl][t][1], a0, (double)v0);
+          }
         }
       }
     }
@@ -876,10 +888,10 @@ static bool tc3_tensor_map(CUtensorMap* map, const float* gy, int B, int d_out) 
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static size_t tc3_smem(int G, int fpb, int rb16) {
-  const size_t ring = (size_t)kTc3Depth * kTc3GBytes + (size_t)kTc3Depth * fpb * tc_rec_bytes(G) +
+static size_t tc3_smem(int G, int fpb, int rb, int nt) {
+  const size_t ring = (size_t)kTc3Depth * (nt / 4) * kTc3BoxBytes + (size_t)kTc3Depth * fpb * tc_rec_bytes(G) +
                       sizeof(double) * (size_t)kTc3Depth * fpb * kTcBC * 4;
-  return 1024 + std::max(ring, sizeof(double) * (size_t)fpb * (4 * rb16 + 4) * 32);  // + alignment slack
+  return 1024 + std::max(ring, sizeof(double) * (size_t)fpb * (4 * rb + 4) * 8 * nt);  // + alignment slack
 }
 
 // tc3 applies to the NT = 4 tc2 shapes (32-output tiles) with 16-byte aligned g rows
@@ -888,14 +900,14 @@ static bool tc3_enabled() {
   return !off;
 }
 
-template <int RB, int FPB, int WPF>
+template <int RB, int NT, int FPB, int WPF>
 static int tc3_launch(const CUtensorMap& map, const float* C, const float* scale, float* dC, float* dscale,
                       unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
                       cudaStream_t st) {
-  auto kern = kan_bwd_tc3_sweep_kernel<RB, FPB, WPF>;
-  const size_t smem = tc3_smem(G, FPB, RB);
+  auto kern = kan_bwd_tc3_sweep_kernel<RB, NT, FPB, WPF>;
+  const size_t smem = tc3_smem(G, FPB, RB, NT);
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 gridd((d_out + 31) / 32, (d_in + FPB - 1) / FPB, p.S);
+  dim3 gridd((d_out + 8 * NT - 1) / (8 * NT), (d_in + FPB - 1) / FPB, p.S);
   kern<<<gridd, FPB * WPF * 32, smem, st>>>(map, recs, C, scale, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
                                             p.nch, p.cps, make_basis<4>(3));
   UKAN_LAUNCH_CHECK();
@@ -944,9 +956,10 @@ static int tc_sweep_dispatch(const float* C, const float* scale, const float* gy
   if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   CUtensorMap map;  // tc3: the driver's tensor-map encoder is required (else the tc2 sweep runs)
-  if (tc3_enabled() && (d_out % 4) == 0 && ((uintptr_t)gy % 16) == 0 && p.split && p.rb == 16 && p.wpf == 4 &&
-      p.nt == 4 && tc3_tensor_map(&map, gy, B, d_out))
-    return tc3_launch<16, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  const bool tc3 = tc3_enabled() && (d_out % 4) == 0 && ((uintptr_t)gy % 16) == 0 && p.split && p.wpf == 4 &&
+                   ((p.rb == 16 && p.nt == 4) || (p.rb == 8 && p.nt == 8)) && tc3_tensor_map(&map, gy, B, d_out);
+  if (tc3 && p.rb == 16) return tc3_launch<16, 4, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (tc3 && p.rb == 8) return tc3_launch<8, 8, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 4) return tc2_launch<16, 4, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8 && p.fpb == 2) return tc2_launch<16, 8, 2, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8) return tc2_launch<16, 4, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
