@@ -259,11 +259,11 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     }
   };
 
-  float acc[SW][OV];
+  float2 acc2[SW][OV / 2];
 #pragma unroll
   for (int s = 0; s < SW; ++s)
 #pragma unroll
-    for (int v = 0; v < OV; ++v) acc[s][v] = 0.f;
+    for (int v = 0; v < OV / 2; ++v) acc2[s][v] = make_float2(0.f, 0.f);
 
   tm_fence_before();
   __syncthreads();  // TMEM address + mbarrier init visible
@@ -319,13 +319,17 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
           w1[j] = b.x; w1[j + 1] = b.y; w1[j + 2] = b.z; w1[j + 3] = b.w;
         }
         tm_wait_ld();
+        // packed FFMA2 over output pairs: each lane of the pair is an IEEE fma, bitwise equal to
+        // two fmaf, at half the issue slots
 #pragma unroll
-        for (int j = 0; j < K; ++j)
+        for (int j = 0; j < K; ++j) {
+          const float2 a0 = make_float2(w0[j], w0[j]), a1 = make_float2(w1[j], w1[j]);
 #pragma unroll
-          for (int v = 0; v < OV; ++v) {
-            acc[s + h][v] = fmaf(w0[j], c0[j * OV + v], acc[s + h][v]);
-            acc[s + h + 1][v] = fmaf(w1[j], c1[j * OV + v], acc[s + h + 1][v]);
+          for (int v = 0; v < OV; v += 2) {
+            acc2[s + h][v / 2] = __ffma2_rn(a0, make_float2(c0[j * OV + v], c0[j * OV + v + 1]), acc2[s + h][v / 2]);
+            acc2[s + h + 1][v / 2] = __ffma2_rn(a1, make_float2(c1[j * OV + v], c1[j * OV + v + 1]), acc2[s + h + 1][v / 2]);
           }
+        }
       }
     }
     __syncwarp();
@@ -354,12 +358,13 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     const int b = b0 + sb + s;
     if (b >= B) continue;
     float* yr = out + (size_t)b * d_out + o;
+    const float av[OV] = {acc2[s][0].x, acc2[s][0].y, acc2[s][1].x, acc2[s][1].y};
     if (o + OV <= d_out && (d_out % OV) == 0) {
-      *reinterpret_cast<float4*>(yr) = make_float4(acc[s][0], acc[s][1], acc[s][2], acc[s][3]);
+      *reinterpret_cast<float4*>(yr) = make_float4(av[0], av[1], av[2], av[3]);
     } else {
 #pragma unroll
       for (int v = 0; v < OV; ++v)
-        if (o + v < d_out) yr[v] = acc[s][v];
+        if (o + v < d_out) yr[v] = av[v];
     }
   }
   tm_fence_before();
