@@ -118,12 +118,15 @@ spline_fwd_kernel(const float* __restrict__ x, const float* __restrict__ T,
         for (int j = 0; j < K; ++j) {
           const float wj = w_s[(f * Bt + s) * K + j];
           const float* q = rp + (size_t)j * d_out;
-          if constexpr (VEC == 4) {
+          if constexpr (VEC == 4) {  // packed FFMA2: bitwise equal to four fmaf
             const float4 cv = __ldg(reinterpret_cast<const float4*>(q));
-            tmp[0] = fmaf(wj, cv.x, tmp[0]);
-            tmp[1] = fmaf(wj, cv.y, tmp[1]);
-            tmp[2] = fmaf(wj, cv.z, tmp[2]);
-            tmp[3] = fmaf(wj, cv.w, tmp[3]);
+            const float2 w2 = make_float2(wj, wj);
+            const float2 t01 = __ffma2_rn(w2, make_float2(cv.x, cv.y), make_float2(tmp[0], tmp[1]));
+            const float2 t23 = __ffma2_rn(w2, make_float2(cv.z, cv.w), make_float2(tmp[2], tmp[3]));
+            tmp[0] = t01.x;
+            tmp[1] = t01.y;
+            tmp[2] = t23.x;
+            tmp[3] = t23.y;
           } else if constexpr (VEC == 2) {
             const float2 cv = __ldg(reinterpret_cast<const float2*>(q));
             tmp[0] = fmaf(wj, cv.x, tmp[0]);
@@ -133,6 +136,17 @@ spline_fwd_kernel(const float* __restrict__ x, const float* __restrict__ T,
           }
         }
         const float sl = has_base ? sl_s[f * Bt + s] : 0.f;
+        if constexpr (VEC == 4) {
+          if (!has_base) {
+            const float2 a01 = __ffma2_rn(make_float2(sc[0], sc[1]), make_float2(tmp[0], tmp[1]), make_float2(acc[r][0], acc[r][1]));
+            const float2 a23 = __ffma2_rn(make_float2(sc[2], sc[3]), make_float2(tmp[2], tmp[3]), make_float2(acc[r][2], acc[r][3]));
+            acc[r][0] = a01.x;
+            acc[r][1] = a01.y;
+            acc[r][2] = a23.x;
+            acc[r][3] = a23.y;
+            continue;
+          }
+        }
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           acc[r][v] = fmaf(sc[v], tmp[v], acc[r][v]);

@@ -11,6 +11,19 @@ from paper_2408_11200_b200 import _lib  # noqa: E402
 from paper_2408_11200_b200._lib import check, ptr, stream_ptr  # noqa: E402
 
 out = sys.argv[1]
+if sys.argv[2] == "ukan":  # UKAN layer forward: python tools/fwd_ab.py OUT.npy ukan B d_in d_out
+    import paper_2408_11200_b200 as P
+    B, d_in, d_out = (int(a) for a in sys.argv[3:6])
+    dev = torch.device("cuda", 0)
+    layer = P.init_layer("ukan", d_in, d_out, 3, seed=0, delta_g=0.5, d_pe=32, d_femb=32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    x = torch.randn((B, d_in), device=dev, generator=g) * 20
+    with torch.no_grad():
+        y = P.ukan_forward(layer, x)
+    np.save(out, y.cpu().numpy())
+    print("saved", out)
+    sys.exit(0)
 B, d_in, d_out, G = (int(a) for a in sys.argv[2:6])
 lib = _lib.load()
 dev = torch.device("cuda", 0)
