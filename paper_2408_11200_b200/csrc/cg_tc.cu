@@ -147,7 +147,7 @@ __device__ __forceinline__ void cg_load_tile(const float* __restrict__ X, int64_
 // accumulators by the threads while the next chunk's MMAs run.  Thread (warp w, lane l) owns
 // row 32*(w%4)+l and columns [(w/4)*BN/2, +BN/2).
 template <int BN, typename AccT, int PIECES>
-__global__ void __launch_bounds__(kTcgThreads, 1)
+__global__ void __launch_bounds__(kTcgThreads, BN <= 64 ? 2 : 1)
 cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const float* __restrict__ Bm, int64_t sbk,
                   int64_t sbn, int M, int N, int K, int kps, int mode, const float* __restrict__ bias, int act,
                   float* __restrict__ C, float* __restrict__ pre, float* __restrict__ part) {
@@ -312,6 +312,207 @@ cg_gemm_tc_kernel(const float* __restrict__ A, int64_t sam, int64_t sak, const f
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
 }
 
+// ---------------------------------------------------------------------------------------
+// Table GEMM with pre-split operands (round 2): C = A B + bias, A [M, K] row-major, B [K, N]
+// row-major, 2 tf32 pieces / 3 products, fp32 promotion per 32-wide K chunk — bitwise the
+// cg_gemm_tc_kernel<BN, float, 2> result, but the operand split is done once per call by
+// cg_presplit_kernel into the canonical K-major core-matrix layout, tile by tile and chunk by
+// chunk, so each (tile, chunk) is one contiguous block: the GEMM then streams them with 1-D bulk
+// copies (cp.async.bulk) through a 3-stage mbarrier ring while the tensor core works, instead of
+// every thread loading, splitting and storing each chunk (the old kernel waited on those loads:
+// long-scoreboard stalls on the split's first instruction, 19% issue).
+//   thread 0: waits chunk c's copies + TMEM buffer c&1 drained (chunk c-2), issues the 12 MMAs,
+//             commits; refills the stage of chunk c-1 with chunk c-1+NS once its MMAs are done;
+//   all:      drain chunk c-1 (TMEM -> fp32 registers), arrive on drained[(c-1)&1].
+
+// Ap[(tile * nch + c) * 2 + piece] = piece of the [ROWS x 32] chunk c of tile `tile` of X, canonical
+// layout; rows / k past the ends are zero.  X(r, k) = X[r * sr + k * sk]; one thread per 4 k (sk == 1)
+// or 4 rows (sr == 1), vectorised along the contiguous dimension.
+template <int ROWS>
+__global__ void __launch_bounds__(256) cg_presplit_kernel(const float* __restrict__ X, int64_t sr, int64_t sk, int R,
+                                                          int K, int nch, unsigned char* __restrict__ out) {
+  constexpr int TB = ROWS * kTcgK * 4;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_chunk = ROWS * kTcgK / 4;  // 4-element groups per (tile, chunk)
+  const int64_t n_tiles = (R + ROWS - 1) / ROWS;
+  if (t >= n_tiles * nch * per_chunk) return;
+  const int g = (int)(t % per_chunk);
+  const int64_t tc = t / per_chunk;
+  const int c = (int)(tc % nch), tile = (int)(tc / nch);
+  unsigned char* dst = out + (size_t)tc * 2 * TB;
+  float e[4];
+  int rr[4], kk[4];
+  if (sk == 1) {  // 4 consecutive k of one row
+    const int r = g / (kTcgK / 4), k = (g % (kTcgK / 4)) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rr[q] = r;
+      kk[q] = k + q;
+    }
+  } else {  // 4 consecutive rows at one k
+    const int k = g / (ROWS / 4), r = (g % (ROWS / 4)) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rr[q] = r + q;
+      kk[q] = k;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int gr = tile * ROWS + rr[q], gk = c * kTcgK + kk[q];
+    e[q] = (gr < R && gk < K) ? __ldg(X + (size_t)gr * sr + (size_t)gk * sk) : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t h = tf32_rna(e[q]);
+    const uint32_t l = tf32_rna(e[q] - __uint_as_float(h));
+    const uint32_t o = cg_off(rr[q], kk[q]);
+    *reinterpret_cast<uint32_t*>(dst + o) = h;
+    *reinterpret_cast<uint32_t*>(dst + TB + o) = l;
+  }
+}
+
+__device__ __forceinline__ void cg_mb_expect_tx(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cg_mb_arrive(uint64_t* mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((uint32_t)__cvta_generic_to_shared(mb)) : "memory");
+}
+__device__ __forceinline__ void cg_bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(mb))
+               : "memory");
+}
+
+template <int BN, int kTpNS>  // kTpNS: smem stages (one K chunk of both operands each)
+__global__ void __launch_bounds__(kTcgThreads, BN <= 64 ? 2 : 1)
+cg_table_tc_kernel(const unsigned char* __restrict__ Ap, const unsigned char* __restrict__ Bp, int M, int N, int nch,
+                   const float* __restrict__ bias, float* __restrict__ C) {
+  constexpr int A_BYTES = kTcgM * kTcgK * 4, B_BYTES = BN * kTcgK * 4;
+  constexpr int STAGE = 2 * (A_BYTES + B_BYTES);  // A hi | A lo | B hi | B lo
+  constexpr int HN = BN / 2;
+  constexpr int TCOLS = 2 * BN;
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(kTcgM >> 4) << 24);  // f32 accum, tf32 A/B, K-major, M=128
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tbase_s;
+  __shared__ __align__(8) uint64_t loaded[kTpNS], mma_done[2], drained[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int nt = blockIdx.x, mt = blockIdx.y;  // n-tiles fastest: a wave shares A tiles through L2
+  const int m0 = mt * kTcgM, n0 = nt * BN;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tbase_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 0) {
+    for (int d = 0; d < kTpNS; ++d) cg_mb_init(&loaded[d], 1);
+    for (int d = 0; d < 2; ++d) {
+      cg_mb_init(&mma_done[d], 1);
+      cg_mb_init(&drained[d], kTcgThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tbase_s;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(half * HN);
+  auto issue = [&](int c) {  // chunk c of both operands -> stage c % NS
+    unsigned char* st = smem_raw + (size_t)(c % kTpNS) * STAGE;
+    uint64_t* mb = &loaded[c % kTpNS];
+    cg_mb_expect_tx(mb, STAGE);
+    cg_bulk_g2s(st, Ap + ((size_t)mt * nch + c) * 2 * A_BYTES, 2 * A_BYTES, mb);
+    cg_bulk_g2s(st + 2 * A_BYTES, Bp + ((size_t)nt * nch + c) * 2 * B_BYTES, 2 * B_BYTES, mb);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < min(kTpNS, nch); ++c) issue(c);
+
+  float acc[HN];
+#pragma unroll
+  for (int j = 0; j < HN; ++j) acc[j] = 0.f;
+  auto drain = [&](int c) {  // chunk c's partial (TMEM buffer c&1) -> registers, then release the buffer
+    cg_mb_wait(&mma_done[c & 1], (uint32_t)((c >> 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t ta = trow + (uint32_t)((c & 1) * BN);
+#pragma unroll
+    for (int cb = 0; cb < HN; cb += 32) {
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(ta + (uint32_t)cb));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (cb + j < HN) acc[cb + j] += __uint_as_float(r[j]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) cg_mb_arrive(&drained[c & 1]);
+  };
+
+  for (int c = 0; c < nch; ++c) {
+    if (threadIdx.x == 0) {
+      cg_mb_wait(&loaded[c % kTpNS], (uint32_t)((c / kTpNS) & 1));
+      if (c >= 2) cg_mb_wait(&drained[c & 1], (uint32_t)(((c - 2) >> 1) & 1));  // TMEM buffer free
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t a0 = sbase + (uint32_t)((c % kTpNS) * STAGE), b0 = a0 + 2 * A_BYTES;
+      const uint32_t td = tmem + (uint32_t)((c & 1) * BN);
+      constexpr int PA2[3] = {0, 1, 0}, PB2[3] = {1, 0, 0};  // (h,l) (l,h) (h,h): as cg_gemm_tc_kernel
+#pragma unroll
+      for (int kk = 0; kk < kTcgK / 8; ++kk) {
+        const uint32_t off = kk * 256;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+          cg_mma_tf32(td, cg_desc(a0 + PA2[t] * A_BYTES + off, 128, 1024), cg_desc(b0 + PB2[t] * B_BYTES + off, 128, 1024),
+                      IDESC, (kk > 0 || t > 0) ? 1 : 0);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&mma_done[c & 1]))
+                   : "memory");
+      // the stage of chunk c-1 is free once its MMAs completed: refill it with chunk c-1+NS
+      if (c >= 1 && c - 1 + kTpNS < nch) {
+        cg_mb_wait(&mma_done[(c - 1) & 1], (uint32_t)(((c - 1) >> 1) & 1));
+        issue(c - 1 + kTpNS);
+      }
+    }
+    __syncwarp();
+    if (c >= 1) drain(c - 1);
+  }
+  if (nch > 0) drain(nch - 1);
+
+  // coalesced epilogue through shared memory (every stage consumed): C = acc + bias
+  constexpr int TS = BN + 1;
+  float* tile = reinterpret_cast<float*>(smem_raw);
+  __syncthreads();
+  const int r = 32 * q + lane;
+#pragma unroll
+  for (int j = 0; j < HN; ++j) {
+    const int n = n0 + half * HN + j;
+    tile[r * TS + half * HN + j] = acc[j] + ((bias && n < N) ? bias[n] : 0.f);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kTcgM * BN; idx += kTcgThreads) {
+    const int rr = idx / BN, cc = idx % BN;
+    const int mm = m0 + rr, n = n0 + cc;
+    if (mm < M && n < N) C[(size_t)mm * N + n] = tile[rr * TS + cc];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
+}
+
 // colsum[n] = sum_k X[k][n] (fp64, fixed order): pass 1 sums 32 columns x one row slice per CTA
 // (8 warps, rows interleaved, then the 8 warp sums in order) into part[slice][n]; pass 2 adds the
 // slices in order.
@@ -402,8 +603,36 @@ int cg_tc_gemm(const float* A, int64_t sam, int64_t sak, const float* Bm, int64_
                int64_t N, int64_t K, int mode, const float* bias, int act, float* C, float* pre, float* part,
                int S, int64_t kps, cudaStream_t st) {
   const int m = (int)M, n = (int)N, k = (int)K, kp = (int)kps;
+  static const bool presplit = !(getenv("UKAN_CG_PRESPLIT") && getenv("UKAN_CG_PRESPLIT")[0] == '0');  // A/B only
+  if (presplit && mode == 0 && act == 0 && S == 1 && sak == 1 && sbn == 1) {
+    // table GEMM: split both operands once into contiguous canonical (tile, chunk) blocks, then
+    // stream them with bulk copies (cg_table_tc_kernel, bitwise the same result)
+    constexpr int BN = 128, NS = 3;  // measured: 0.83 ms at the cfg4 shape vs 0.89 ms for BN 64 x 2 stages x 2 CTAs/SM
+    const int nch = (k + kTcgK - 1) / kTcgK;
+    const int64_t mt = (M + kTcgM - 1) / kTcgM, ntl = (N + BN - 1) / BN;
+    const size_t a_bytes = (size_t)mt * nch * 2 * kTcgM * kTcgK * 4, b_bytes = (size_t)ntl * nch * 2 * BN * kTcgK * 4;
+    void* buf = nullptr;
+    UKAN_CUDA_TRY(scratch_alloc(&buf, a_bytes + b_bytes, st));
+    unsigned char* ap = static_cast<unsigned char*>(buf);
+    unsigned char* bp = ap + a_bytes;
+    const int64_t na = mt * nch * (kTcgM * kTcgK / 4), nb = ntl * nch * (BN * kTcgK / 4);
+    cg_presplit_kernel<kTcgM><<<(unsigned)((na + 255) / 256), 256, 0, st>>>(A, sam, sak, m, k, nch, ap);
+    UKAN_LAUNCH_CHECK();
+    cg_presplit_kernel<BN><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(Bm, sbn, sbk, n, k, nch, bp);
+    UKAN_LAUNCH_CHECK();
+    auto kern = cg_table_tc_kernel<BN, NS>;
+    const size_t smem = std::max<size_t>((size_t)NS * 2 * (kTcgM + BN) * kTcgK * 4, (size_t)kTcgM * (BN + 1) * 4) + 1024;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<dim3((unsigned)ntl, (unsigned)mt), kTcgThreads, smem, st>>>(ap, bp, m, n, nch, bias, C);
+    UKAN_LAUNCH_CHECK();
+    cudaFreeAsync(buf, st);
+    return UKAN_OK;
+  }
   // Only the table GEMM (mode 0, act 0) takes this path: its outputs feed the spline forward, where
   // fp32-level accuracy keeps parity — two tf32 pieces (3 products), fp32 promotion registers.
+  static const int bn_env = getenv("UKAN_CG_BN") ? atoi(getenv("UKAN_CG_BN")) : 0;  // A/B measurement only
+  if (bn_env == 64) return cg_launch<64, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
+  if (bn_env == 128) return cg_launch<128, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
   if (N >= 256 && (M + kTcgM - 1) / kTcgM * (N / 256) >= kan_num_sms())
     return cg_launch<256, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
   if (N > 64) return cg_launch<128, float, 2>(A, sam, sak, Bm, sbk, sbn, m, n, k, kp, S, mode, bias, act, C, pre, part, st);
