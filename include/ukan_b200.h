@@ -251,6 +251,21 @@ int ukan_ukan_backward(const float* x, const int32_t* base_row, const int32_t* s
                        double delta_g, void* workspace, int64_t workspace_bytes,
                        void* stream);
 
+/* Dense UKAN layers (every feature's virtual table has max_rows <= 67 rows, k = 3, d_out >= 64,
+ * d_out % 4 == 0): the same gradients as ukan_ukan_backward (layers.py:254-291 backward) on the
+ * KAN FP64 tensor-core backward — cell-sorted records per (feature, 256-sample chunk), the banded
+ * DMMA table-gradient sweep writing each feature's row segment of dtable (or, for segments of
+ * fewer than 24 rows, the sorted-merge sweep of ukan_ukan_backward), and the DMMA dx.
+ * max_rows is the *max_rows_host of ukan_ukan_build_keys.  The workspace size is 0 when the layer
+ * does not qualify (call ukan_ukan_backward then).  Deterministic. */
+int64_t ukan_ukan_backward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
+                                                int64_t max_rows, int k);
+int ukan_ukan_backward_dense(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                             const float* table, const float* scale, const float* gy,
+                             float* dx, float* dtable, float* dscale,
+                             int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int64_t max_rows, int k,
+                             double delta_g, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Forward tangent of the UKAN spline over the generated table (u = x/dg - g_id carries tx/dg,
  * layers.py:264; the table has no tangent) and its backward: dx (tangent share, nullable), dtx
  * (nullable), dtable [n_u*K, d_out] (written), dscale (written).  Same key layout as above. */

@@ -54,9 +54,14 @@ __device__ __forceinline__ unsigned tc_same_cell_mask(int cell) {
   return eq;
 }
 
+// UK: a dense UKAN layer (every feature's virtual table has <= G + 3 rows): the cell is the
+// sample's window start inside its feature's row segment, base_row[b, i] - 4 * seg[i]
+// (layers.py:261-287), u = x/dg - floor(x/dg) (layers.py:263), never clamped.
+template <bool UK>
 __global__ void __launch_bounds__(256)
 kan_bwd_tc_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ recs, int B, int d_in,
-                       int nch, int G, KanGrid grid) {
+                       int nch, int G, KanGrid grid, const int32_t* __restrict__ base_row,
+                       const int32_t* __restrict__ seg, double inv_dg) {
   __shared__ float xs[kTcBC][9];
   __shared__ int cnt[8][80];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -91,7 +96,16 @@ kan_bwd_tc_prep_kernel(const float* __restrict__ x, unsigned char* __restrict__ 
     int cell = -1;
     double u = 0.0;
     bool mask = true;
-    if (s < nb) kan_locate(xs[s][warp], grid, cell, u, mask);
+    if constexpr (UK) {
+      if (s < nb) {
+        int64_t gid;
+        ukan_locate(xs[s][warp], inv_dg, gid, u);
+        cell = base_row[(size_t)(b0 + s) * d_in + i] - 4 * seg[i];
+        if (cell < 0 || cell > G - 1 || !(u == u)) cell = -1;  // outside the plan (never for valid keys)
+      }
+    } else {
+      if (s < nb) kan_locate(xs[s][warp], grid, cell, u, mask);
+    }
     if (!mask) clamped |= 1u << q;
     cells[q] = cell;
     us[q] = u;
@@ -551,7 +565,7 @@ __global__ void __launch_bounds__(FPB * WPF * 32, 1)
 kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigned char* __restrict__ recs,
                          const float* __restrict__ C, const float* __restrict__ scale, float* __restrict__ dC,
                          float* __restrict__ dscale, double* __restrict__ part, int B, int d_in, int d_out, int G,
-                         int nch, int cps, Basis<4> bas) {
+                         int nch, int cps, Basis<4> bas, const int32_t* __restrict__ seg) {
   constexpr int OPB = 8 * NT, NBOX = OPB / 32;
   constexpr uint32_t kTc3GBytes = NBOX * kTc3BoxBytes;  // one g stage: 256 samples x OPB outputs
   static_assert(NT == 4 || NT == 8, "32-output TMA boxes");
@@ -719,13 +733,18 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
     const int ii = i0 + f, o = o0 + oc;
     if (ii >= d_in || o >= d_out) continue;
     const double* Sf = S + (size_t)f * RR * OPB + oc;
+    int rbase = ii * R, nr = R;  // UKAN: the feature's own row segment of the table
+    if (seg != nullptr) {
+      rbase = 4 * seg[ii];
+      nr = 4 * seg[ii + 1] - rbase;
+    }
     if (part != nullptr) {
       for (int r = 0; r < R; ++r) part[(size_t)z * d_in * R * d_out + ((size_t)ii * R + r) * d_out + o] = Sf[(size_t)r * OPB];
     } else {
       const double sc = (double)scale[(size_t)ii * d_out + o];
       double ds = 0.0;
-      for (int r = 0; r < R; ++r) {
-        const size_t ci = ((size_t)ii * R + r) * d_out + o;
+      for (int r = 0; r < nr; ++r) {
+        const size_t ci = ((size_t)rbase + r) * d_out + o;
         const double a = Sf[(size_t)r * OPB];
         dC[ci] = (float)(sc * a);
         ds = fma((double)C[ci], a, ds);
@@ -742,17 +761,20 @@ __global__ void __launch_bounds__(256) kan_bwd_tc_reduce_kernel(const double* __
                                                                 const float* __restrict__ C,
                                                                 const float* __restrict__ scale,
                                                                 float* __restrict__ dC, float* __restrict__ dscale,
-                                                                int S, int d_in, int d_out, int R) {
+                                                                int S, int d_in, int d_out, int R,
+                                                                const int32_t* __restrict__ seg = nullptr) {
   extern __shared__ double prod[];  // [R][32]
   const int i = blockIdx.x, o0 = blockIdx.y * 32;
   const size_t zs = (size_t)d_in * R * d_out;
+  // the partials use the padded [d_in][R] row layout; dC / C rows: the feature's segment (UKAN)
+  const int rbase = seg ? 4 * seg[i] : i * R, nr = seg ? 4 * (seg[i + 1] - seg[i]) : R;
   for (int p = threadIdx.x; p < R * 32; p += blockDim.x) {
     const int r = p >> 5, ol = p & 31, o = o0 + ol;
     double pr = 0.0;
-    if (o < d_out) {
-      const size_t ci = ((size_t)i * R + r) * d_out + o;
+    if (o < d_out && r < nr) {
+      const size_t pi = ((size_t)i * R + r) * d_out + o, ci = ((size_t)rbase + r) * d_out + o;
       double a = 0.0;
-      for (int z = 0; z < S; ++z) a += part[z * zs + ci];
+      for (int z = 0; z < S; ++z) a += part[z * zs + pi];
       dC[ci] = (float)((double)scale[(size_t)i * d_out + o] * a);
       pr = (double)C[ci] * a;
     }
@@ -903,17 +925,17 @@ static bool tc3_enabled() {
 template <int RB, int NT, int FPB, int WPF>
 static int tc3_launch(const CUtensorMap& map, const float* C, const float* scale, float* dC, float* dscale,
                       unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int32_t* seg = nullptr) {
   auto kern = kan_bwd_tc3_sweep_kernel<RB, NT, FPB, WPF>;
   const size_t smem = tc3_smem(G, FPB, RB, NT);
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 gridd((d_out + 8 * NT - 1) / (8 * NT), (d_in + FPB - 1) / FPB, p.S);
   kern<<<gridd, FPB * WPF * 32, smem, st>>>(map, recs, C, scale, dC, dscale, p.S > 1 ? part : nullptr, B, d_in, d_out, G,
-                                            p.nch, p.cps, make_basis<4>(3));
+                                            p.nch, p.cps, make_basis<4>(3), seg);
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
     kan_bwd_tc_reduce_kernel<<<dim3(d_in, (d_out + 31) / 32), 256, sizeof(double) * (G + 3) * 32, st>>>(
-        part, C, scale, dC, dscale, p.S, d_in, d_out, G + 3);
+        part, C, scale, dC, dscale, p.S, d_in, d_out, G + 3, seg);
     UKAN_LAUNCH_CHECK();
   }
   return UKAN_OK;
@@ -943,7 +965,8 @@ int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, in
                     const TcPlan& p, cudaStream_t st) {
   if (!p.ok || workspace == nullptr || ws_bytes < kan_bwd_tc_workspace(p)) return UKAN_E_WORKSPACE;
   dim3 pg((d_in + 7) / 8, p.nch);
-  kan_bwd_tc_prep_kernel<<<pg, 256, 0, st>>>(x, reinterpret_cast<unsigned char*>(workspace), B, d_in, p.nch, G, grid);
+  kan_bwd_tc_prep_kernel<false><<<pg, 256, 0, st>>>(x, reinterpret_cast<unsigned char*>(workspace), B, d_in, p.nch, G,
+                                                     grid, nullptr, nullptr, 0.0);
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
 }
@@ -1098,10 +1121,11 @@ template <int kDxW, int MAXT>
 __global__ void __launch_bounds__(kDxW * 32, 1)
 kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C, const float* __restrict__ scale,
                  const float* __restrict__ gy, float* __restrict__ dx, int B, int d_in, int d_out, int G, int nch,
-                 int n_fg, int band, int ld, double inv_dg, Basis<4> bas) {
+                 int n_fg, int band, int ld, double inv_dg, Basis<4> bas, const int32_t* __restrict__ seg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double Msh[16];
   __shared__ int cnt_s[kDxF];
+  __shared__ int rbase_s[kDxF], nr_s[kDxF];  // each feature's row segment (UKAN: its own slice of the table)
   const DxSmem L = dx_smem_layout(G);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, kq = lane & 3;
@@ -1121,6 +1145,12 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   const int i0 = fg * kDxF;
   const int b0 = n * kTcBC;
   const int nb = min(kTcBC, B - b0);
+  if (threadIdx.x < kDxF) {
+    const int ii = min(i0 + (int)threadIdx.x, d_in - 1);
+    rbase_s[threadIdx.x] = seg ? 4 * seg[ii] : ii * (G + 3);
+    nr_s[threadIdx.x] = seg ? 4 * (seg[ii + 1] - seg[ii]) : G + 3;
+  }
+  __syncthreads();
   unsigned char* rec_s = smem_raw + L.rec;
   int4* task_s = reinterpret_cast<int4*>(smem_raw + L.task);
   float* g_s = reinterpret_cast<float*>(smem_raw + L.g);
@@ -1157,8 +1187,8 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
       const int t = threadIdx.x + q * kDxW * 32;
       const int j = (t % nq) * 4, fr = t / nq, r = fr % RR, f = fr / RR;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (f < kDxF && r < R && i0 + f < d_in && o0 + j < d_out)
-        v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)(i0 + f) * R + r) * d_out + o0 + j));
+      if (f < kDxF && i0 + f < d_in && r < nr_s[f] && o0 + j < d_out)
+        v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)rbase_s[f] + r) * d_out + o0 + j));
       cr[q] = v;
     }
   };
@@ -1308,7 +1338,8 @@ bool kan_dx_tc_applicable(const TcPlan& p, const float* C, const float* gy, int 
 // dx from the records kan_bwd_tc_prep left in `recs` (features [0, d_in) of the pointers given;
 // dx rows have stride ld).
 static int dx_tc_launch(const float* C, const float* scale, const float* gy, float* dx, const unsigned char* recs,
-                        int B, int d_in, int d_out, int G, int nch, int ld, const KanGrid& grid, cudaStream_t st) {
+                        int B, int d_in, int d_out, int G, int nch, int ld, const KanGrid& grid, cudaStream_t st,
+                        const int32_t* seg = nullptr) {
   const DxSmem L = dx_smem_layout(G);
   const int n_fg = (d_in + kDxF - 1) / kDxF;
   // band 8: least DRAM traffic at cfg3 (45.8 GB per call at B = 16384 vs 72 GB at 16, 192 GB at 32;
@@ -1321,12 +1352,12 @@ static int dx_tc_launch(const float* C, const float* scale, const float* gy, flo
     auto kern = kan_dx_tc_kernel<16, 12>;
     UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<(unsigned)nblk, 16 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
-                                                   grid.inv_dg, make_basis<4>(3));
+                                                   grid.inv_dg, make_basis<4>(3), seg);
   } else {
     auto kern = kan_dx_tc_kernel<32, 6>;
     UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<(unsigned)nblk, 32 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
-                                                   grid.inv_dg, make_basis<4>(3));
+                                                   grid.inv_dg, make_basis<4>(3), seg);
   }
   UKAN_LAUNCH_CHECK();
   return UKAN_OK;
@@ -1370,6 +1401,58 @@ int kan_bwd_tc_part(const float* C, const float* scale, const float* gy, float* 
     if (!kan_dx_tc_applicable(full, C, gy, d_out, G)) return UKAN_E_ARG;
     return dx_tc_launch(C + (size_t)i_lo * R * d_out, scale + (size_t)i_lo * d_out, gy, dx + i_lo, recs, B, n, d_out,
                         G, full.nch, d_in, grid, st);
+  }
+  return UKAN_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Dense UKAN layers on the KAN tensor-core backward (round 2).  When every feature's virtual
+// table has <= 67 rows (cfg5: <= 32), a 256-sample chunk piles up on a few dozen rows, exactly the
+// regime of the banded DMMA sweep and dx above; the UKAN table is then "a KAN table whose feature
+// i owns rows [4 seg[i], 4 seg[i+1])".  Records: kan_bwd_tc_prep_kernel<true> (cell = window start
+// inside the segment, UKAN u); table gradient: the tc3 sweep writing dT rows of the segment;
+// dx: kan_dx_tc_kernel staging C' from the segment.  Replaces the sorted-merge sweep
+// (seg_fsweep) and the per-pair dx (spline_dx64) for those layers, layers.py:254-291.
+static int ukan_dense_G(int64_t max_rows) { return (int)std::max<int64_t>(17, max_rows - 3); }
+
+int64_t ukan_dense_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k) {
+  static const bool off = getenv("UKAN_UKAN_DENSE") && getenv("UKAN_UKAN_DENSE")[0] == '0';  // A/B only
+  if (off || k != 3 || B < 1 || max_rows < 1 || max_rows > 67 || d_out < 64 || d_out % 4 || !tc3_enabled()) return 0;
+  const TcPlan p = kan_bwd_tc_plan(B, d_in, d_out, ukan_dense_G(max_rows), 3, false);
+  if (!p.ok || !p.split || p.wpf != 4) return 0;
+  return kan_bwd_tc_workspace(p);  // records + split-K partials (padded [d_in][G+3] rows)
+}
+
+int ukan_dense_backward(const float* x, const int32_t* base_row, const int32_t* seg, const float* T,
+                        const float* scale, const float* gy, float* dx, float* dT, float* dscale, int B, int d_in,
+                        int d_out, int64_t max_rows, double delta_g, void* ws, int64_t ws_bytes, cudaStream_t st,
+                        bool table) {
+  const int64_t need = ukan_dense_workspace(B, d_in, d_out, max_rows, 3);
+  if (need <= 0 || ws == nullptr || ws_bytes < need) return UKAN_E_WORKSPACE;
+  const int G = ukan_dense_G(max_rows);
+  const TcPlan p = kan_bwd_tc_plan(B, d_in, d_out, G, 3, false);
+  unsigned char* recs = static_cast<unsigned char*>(ws);
+  double* part = reinterpret_cast<double*>(recs + ((p.rec_bytes + 255) / 256) * 256);
+  KanGrid grid{};
+  grid.inv_dg = 1.0 / delta_g;
+  grid.G = G;
+  if (!table && dx == nullptr) return UKAN_OK;  // the caller computed dT / dscale; no dx wanted
+  dim3 pg((d_in + 7) / 8, p.nch);
+  kan_bwd_tc_prep_kernel<true><<<pg, 256, 0, st>>>(x, recs, B, d_in, p.nch, G, grid, base_row, seg, grid.inv_dg);
+  UKAN_LAUNCH_CHECK();
+  if (table) {  // else the caller computed dT / dscale (sorted-merge sweep)
+    CUtensorMap map;
+    if (!((uintptr_t)gy % 16 == 0 && tc3_tensor_map(&map, gy, B, d_out))) return UKAN_E_ARG;
+    int rc = UKAN_E_ARG;
+    if (p.rb == 16 && p.nt == 4)
+      rc = tc3_launch<16, 4, 4, 4>(map, T, scale, dT, dscale, recs, part, B, d_in, d_out, G, p, st, seg);
+    else if (p.rb == 8 && p.nt == 8)
+      rc = tc3_launch<8, 8, 4, 4>(map, T, scale, dT, dscale, recs, part, B, d_in, d_out, G, p, st, seg);
+    if (rc) return rc;
+  }
+  if (dx) {
+    if (((uintptr_t)T % 16) != 0) return UKAN_E_ARG;
+    return dx_tc_launch(T, scale, gy, dx, recs, B, d_in, d_out, G, p.nch, d_in, grid, st, seg);
   }
   return UKAN_OK;
 }

@@ -558,6 +558,12 @@ TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
 // kan_small.cu: small layers (d_in * d_out <= 2^14, k = 3, no base branch)
 bool kan_small_ok(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k, bool has_base);
 int64_t kan_small_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t G);
+// kan_bwd_tc.cu: dense UKAN layers on the KAN tensor-core backward
+int64_t ukan_dense_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k);
+int ukan_dense_backward(const float* x, const int32_t* base_row, const int32_t* seg, const float* T,
+                        const float* scale, const float* gy, float* dx, float* dT, float* dscale, int B, int d_in,
+                        int d_out, int64_t max_rows, double delta_g, void* ws, int64_t ws_bytes, cudaStream_t st,
+                        bool table);
 int kan_small_forward(const float* x, const float* C, const float* scale, float* y, int B, int d_in, int d_out, int G,
                       const KanGrid& grid, int32_t* err, cudaStream_t st);
 int kan_small_records(const float* x, void* ws, int B, int d_in, const KanGrid& grid, cudaStream_t st);
@@ -1064,6 +1070,55 @@ extern "C" int64_t ukan_ukan_backward_workspace_size(int64_t B, int64_t d_in, in
   if (ukan_seg_ok(B, d_out, k) && getenv("UKAN_UKAN_BWD") == nullptr)
     return ((seg_workspace(B, d_in, d_out, n_u * (k + 1)) + 255) / 256) * 256 + ukan_dx64_bytes(B, d_in, d_out);
   return (int64_t)sizeof(double) * n_u * (k + 1) * d_out;
+}
+
+// Dense UKAN layers: the table gradient on the banded DMMA sweep when the features' segments have
+// enough rows to keep its four warps per feature busy, else on the sorted-merge sweep (seg_*),
+// whose warps are not tied to row blocks (cfg5 layers with <= 12 rows: 13.7 vs 15.3 ms); dx
+// always on the DMMA dx.  A/B: UKAN_DENSE_SWEEP_MIN_ROWS.
+static bool ukan_dense_sweep(int64_t max_rows) {
+  static const int64_t min_rows = getenv("UKAN_DENSE_SWEEP_MIN_ROWS") ? atoll(getenv("UKAN_DENSE_SWEEP_MIN_ROWS")) : 24;
+  return max_rows >= min_rows;
+}
+
+extern "C" int64_t ukan_ukan_backward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
+                                                          int64_t max_rows, int k) {
+  if (B < 1 || d_in < 1 || d_out < 1 || B > INT32_MAX || n_u < 1 || n_u * (k + 1) >= ((int64_t)1 << 31)) return 0;
+  const int64_t tc = ukan_dense_workspace(B, d_in, d_out, max_rows, k);
+  if (tc <= 0 || ukan_dense_sweep(max_rows)) return tc;
+  if (!ukan_seg_ok(B, d_out, k)) return 0;
+  return ((tc + 255) / 256) * 256 + seg_workspace(B, d_in, d_out, n_u * (k + 1));
+}
+
+extern "C" int ukan_ukan_backward_dense(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                                        const float* table, const float* scale, const float* gy, float* dx,
+                                        float* dtable, float* dscale, int64_t B, int64_t d_in, int64_t d_out,
+                                        int64_t n_u, int64_t max_rows, int k, double delta_g, void* workspace,
+                                        int64_t workspace_bytes, void* stream) {
+  if (k != 3) return UKAN_E_DEGREE;
+  if (!(delta_g > 0)) return UKAN_E_GRID;
+  if (!x || !base_row || !seg_start || !table || !scale || !gy || !dtable || !dscale || B < 1 || d_in < 1 ||
+      d_out < 1 || B > INT32_MAX)
+    return UKAN_E_ARG;
+  const int64_t need = ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, n_u, max_rows, k);
+  if (need <= 0) return UKAN_E_ARG;
+  if (workspace == nullptr || workspace_bytes < need) return UKAN_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t tc = ukan_dense_workspace(B, d_in, d_out, max_rows, k);
+  const bool sweep = ukan_dense_sweep(max_rows);
+  if (!sweep) {  // table gradient on the sorted-merge sweep, in the workspace after the records
+    RowMap rm{};
+    rm.inv_dg = 1.0 / delta_g;
+    rm.base_row = base_row;
+    rm.seg_start = seg_start;
+    rm.K = k + 1;
+    const int64_t off = ((tc + 255) / 256) * 256;
+    const int rc = seg_table_grad<4, true>(x, table, scale, gy, dtable, dscale, static_cast<unsigned char*>(workspace) + off,
+                                           workspace_bytes - off, (int)B, (int)d_in, (int)d_out, n_u * (k + 1), rm, st);
+    if (rc) return rc;
+  }
+  return ukan_dense_backward(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, (int)B, (int)d_in,
+                             (int)d_out, max_rows, delta_g, workspace, tc, st, sweep);
 }
 
 extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,

@@ -209,7 +209,7 @@ def ukan_forward(layer: UkanLayer, x, dedup: bool = True) -> torch.Tensor:
     keys = ops.ukan_build_keys(x.detach(), layer.k, float(layer.delta_g))
     table = _cg_table(layer, keys)
     return ops.UkanSplineFn.apply(x, table, layer.scale, keys.base_row, keys.seg_start, layer.k,
-                                  float(layer.delta_g))
+                                  float(layer.delta_g), keys.max_rows)
 
 
 def kan_forward_tangent(layer: KanLayer, x, tx):
@@ -236,7 +236,8 @@ def ukan_forward_tangent(layer: UkanLayer, x, tx, dedup: bool = True):
         raise DimensionError(f"tangent seed shape {tuple(tx.shape)} != {tuple(x.shape)}")
     keys = ops.ukan_build_keys(x.detach(), layer.k, float(layer.delta_g))
     table = _cg_table(layer, keys)
-    y = ops.UkanSplineFn.apply(x, table, layer.scale, keys.base_row, keys.seg_start, layer.k, float(layer.delta_g))
+    y = ops.UkanSplineFn.apply(x, table, layer.scale, keys.base_row, keys.seg_start, layer.k, float(layer.delta_g),
+                               keys.max_rows)
     ty = ops.UkanJvpFn.apply(x, tx, table, layer.scale, keys.base_row, keys.seg_start, layer.k,
                              float(layer.delta_g))
     return y, ty

@@ -291,7 +291,7 @@ class UkanSplineFn(torch.autograd.Function):
     """Spline evaluation over the generated table (layers.py:284-291)."""
 
     @staticmethod
-    def forward(ctx, x, table, scale, base_row, seg_start, k: int, delta_g: float):
+    def forward(ctx, x, table, scale, base_row, seg_start, k: int, delta_g: float, max_rows: int = 0):
         lib = _lib.load()
         _lib.require_cuda(x, table, scale)
         _lib.require_params(x.device, table, scale)
@@ -302,27 +302,43 @@ class UkanSplineFn(torch.autograd.Function):
         check(lib.ukan_ukan_forward(ptr(x), ptr(base_row), ptr(table), ptr(scale), ptr(y), B, d_in, d_out, k,
                                     delta_g, stream_ptr()), "ukan_forward")
         ctx.save_for_backward(x, table, scale, base_row, seg_start)
-        ctx.meta = (k, float(delta_g))
+        ctx.meta = (k, float(delta_g), int(max_rows))
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        lib = _lib.load()
         x, table, scale, base_row, seg_start = ctx.saved_tensors
-        k, delta_g = ctx.meta
+        k, delta_g, max_rows = ctx.meta
         gy = _f32(gy)
-        B, d_in = x.shape
-        d_out = scale.shape[1]
-        n_u = table.shape[0]
         dx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
         dtable = torch.empty_like(table)
         ds = torch.empty_like(scale)
-        nbytes = lib.ukan_ukan_backward_workspace_size(B, d_in, d_out, n_u, k)
-        ws = torch.empty(max(nbytes, 8), device=x.device, dtype=torch.uint8)
-        check(lib.ukan_ukan_backward(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(gy),
-                                     ptr(dx), ptr(dtable), ptr(ds), B, d_in, d_out, n_u, k, delta_g, ptr(ws),
-                                     nbytes, stream_ptr()), "ukan_backward")
-        return dx, dtable, ds, None, None, None, None
+        ukan_backward_into(x, base_row, seg_start, table, scale, gy, dx, dtable, ds, k, delta_g, max_rows)
+        return dx, dtable, ds, None, None, None, None, None
+
+
+def ukan_backward_into(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, k: int, delta_g: float,
+                       max_rows: int = 0) -> None:
+    """dx (optional), dtable, dscale of the UKAN spline (layers.py:284-291 backward).  Dense layers
+    (every feature's virtual table <= 67 rows: max_rows from ukan_build_keys) take the KAN FP64
+    tensor-core backward (ukan_ukan_backward_dense); the others the sorted-merge sweep."""
+    lib = _lib.load()
+    B, d_in = x.shape
+    d_out = scale.shape[1]
+    n_u = table.shape[0]
+    st = stream_ptr()
+    nbytes = lib.ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, n_u, max_rows, k) if max_rows > 0 else 0
+    if nbytes > 0:
+        ws = torch.empty(nbytes, device=x.device, dtype=torch.uint8)
+        check(lib.ukan_ukan_backward_dense(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(gy),
+                                           ptr(dx), ptr(dtable), ptr(dscale), B, d_in, d_out, n_u, max_rows, k, delta_g,
+                                           ptr(ws), nbytes, st), "ukan_backward_dense")
+        return
+    nbytes = lib.ukan_ukan_backward_workspace_size(B, d_in, d_out, n_u, k)
+    ws = torch.empty(max(nbytes, 8), device=x.device, dtype=torch.uint8)
+    check(lib.ukan_ukan_backward(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(gy), ptr(dx),
+                                 ptr(dtable), ptr(dscale), B, d_in, d_out, n_u, k, delta_g, ptr(ws), nbytes, st),
+          "ukan_backward")
 
 
 class KanJvpFn(torch.autograd.Function):

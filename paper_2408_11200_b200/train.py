@@ -204,12 +204,8 @@ class SplineTrainer:
         keys, cg_cache, table = cache
         n_u = keys.n_u
         dtable = torch.empty_like(table)
-        nbytes = self.lib.ukan_ukan_backward_workspace_size(B, layer.d_in, layer.d_out, n_u, layer.k)
-        ws = torch.empty(max(nbytes, 8), device=self.device, dtype=torch.uint8)
-        check(self.lib.ukan_ukan_backward(ptr(h), ptr(keys.base_row), ptr(keys.seg_start), ptr(table),
-                                          ptr(layer.scale), ptr(gy), ptr(dx), ptr(dtable), ptr(gv[pre_ + "scale"]),
-                                          B, layer.d_in, layer.d_out, n_u, layer.k, float(layer.delta_g), ptr(ws),
-                                          nbytes, st), "ukan_backward")
+        ops.ukan_backward_into(h, keys.base_row, keys.seg_start, table, layer.scale, gy, dx, dtable,
+                               gv[pre_ + "scale"], layer.k, float(layer.delta_g), keys.max_rows)
         ops.cg_backward_raw(cg_cache, dtable, layer.cg_w1, layer.cg_w2, keys.seg_start, layer.d_femb,
                             gv[pre_ + "cg_w1"], gv[pre_ + "cg_b1"], gv[pre_ + "cg_w2"], gv[pre_ + "cg_b2"],
                             gv[pre_ + "feature_embedding"])

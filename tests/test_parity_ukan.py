@@ -173,3 +173,49 @@ def test_ukan_segmented_sweep_multi_chunk(d_out, sigma):
     b = run(layer, x, gup)
     for key in a:
         np.testing.assert_array_equal(a[key], b[key])
+
+
+@pytest.mark.parametrize("B,d_in,d_out,dg,sigma", [(1500, 12, 64, 0.4, 1.0), (700, 9, 100, 1.0, 7.0), (257, 33, 256, 0.5, 2.0),
+                                                  (2000, 16, 64, 0.4, 0.3)])
+def test_ukan_dense_layer_on_tensor_cores(B, d_in, d_out, dg, sigma):
+    """Dense UKAN layers (every feature's virtual table <= 67 rows, the cfg5 regime) take the KAN
+    FP64 tensor-core backward (ukan_ukan_backward_dense): multi-chunk, ragged output tiles
+    (d_out = 100), 8- and 16-row-block plans, few-row segments (sorted-merge table sweep + DMMA
+    dx); oracle parity and bitwise determinism."""
+    from paper_2408_11200_b200 import _lib
+    layer, x, gup = random_case(B, d_in, d_out, 3, dg, 8, 8, seed=B + d_out, sigma=sigma)
+    keys = ops.ukan_build_keys(_t(x), 3, dg)
+    assert 0 < keys.max_rows <= 67
+    assert _lib.load().ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, keys.n_u, keys.max_rows, 3) > 0
+    check_against_oracle(layer, x, gup)
+    for p in layer.parameters().values():
+        p.grad = None
+    a = run(layer, x, gup)
+    for p in layer.parameters().values():
+        p.grad = None
+    b = run(layer, x, gup)
+    for key in a:
+        np.testing.assert_array_equal(a[key], b[key])
+
+
+def test_ukan_dense_stack_training_step():
+    """A cfg5-shaped (scaled-down) UKAN stack through SplineTrainer: layers 1 and 2 are dense and
+    need dx; the step's gradients match oracle.model_step."""
+    widths, dg = [8, 64, 64], 0.4
+    kw = dict(delta_g=dg, d_pe=8, d_femb=8)
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=(700, widths[0])).astype(np.float32)
+    t = rng.normal(size=(700, widths[-1])).astype(np.float32)
+    model = P.build_model("ukan", widths, 3, seed=0, device=DEV, **kw)
+    params = [{n: v.detach().double().cpu().numpy() for n, v in L.parameters().items()} for L in model.layers]
+    tr = P.SplineTrainer(model, "mse", 1e-3, "adam")
+    tr.read_loss(tr.step(torch.tensor(x, device=DEV), torch.tensor(t, device=DEV)))
+    grad = tr.flat.grad.cpu().numpy()
+    cfgs = [dict(k=3, delta_g=dg, d_pe=8) for _ in model.layers]
+    _, want, _, _, _ = oracle.model_step("ukan", params, cfgs, x.astype(np.float64), t.astype(np.float64), "mse", 1e-3)
+    off = 0
+    for li, L in enumerate(model.layers):
+        for n, v in L.parameters().items():
+            g = grad[off:off + v.numel()].reshape(v.shape)
+            off += v.numel()
+            assert_close(g, want[li][n], what=f"layer{li}.{n}")
