@@ -560,7 +560,11 @@ static __device__ __forceinline__ void tc_tma_2d(void* smem, const CUtensorMap* 
 constexpr int kTc3Depth = 2;
 constexpr uint32_t kTc3BoxBytes = kTcBC * 32 * 4;  // one TMA box: 256 samples x 32 outputs fp32
 
-template <int RB, int NT, int FPB, int WPF>
+// SS ("sample split", few-row dense UKAN segments): each of a feature's WPF warps takes a quarter
+// of the chunk's sorted positions over ALL RB blocks instead of RB/WPF blocks over all positions,
+// so a handful of populated blocks still keeps every warp busy; the warps' partial rows meet in
+// the epilogue in warp order (deterministic; the 4-sample grouping differs from SS = false).
+template <int RB, int NT, int FPB, int WPF, bool SS = false>
 __global__ void __launch_bounds__(FPB * WPF * 32, 1)
 kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigned char* __restrict__ recs,
                          const float* __restrict__ C, const float* __restrict__ scale, float* __restrict__ dC,
@@ -569,7 +573,7 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
   constexpr int OPB = 8 * NT, NBOX = OPB / 32;
   constexpr uint32_t kTc3GBytes = NBOX * kTc3BoxBytes;  // one g stage: 256 samples x OPB outputs
   static_assert(NT == 4 || NT == 8, "32-output TMA boxes");
-  constexpr int BH = RB / WPF;
+  constexpr int BH = SS ? RB : RB / WPF;  // blocks per warp
   constexpr int NWARP = FPB * WPF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_s[kTc3Depth], empty_s[kTc3Depth];
@@ -640,8 +644,9 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
       const int* ent = reinterpret_cast<const int*>(rec);
       const double* uu = reinterpret_cast<const double*>(rec + kTcBC * 4);
       const int* st = reinterpret_cast<const int*>(rec + kTcBC * 12);
-      // this warp's sorted positions: the cells of its blocks [h*BH, (h+1)*BH)
-      const int p_lo = st[min(4 * h * BH, G)], p_hi = st[min(4 * (h + 1) * BH, G)];
+      // this warp's sorted positions: the cells of its blocks [h*BH, (h+1)*BH), or (SS) its quarter
+      const int p_lo = SS ? min(h * (kTcBC / WPF), st[G]) : st[min(4 * h * BH, G)];
+      const int p_hi = SS ? min((h + 1) * (kTcBC / WPF), st[G]) : st[min(4 * (h + 1) * BH, G)];
       for (int p = p_lo + lane; p < p_hi; p += 32) {  // fp64 Horner, layers.py:29-37
         const double u = uu[p];
         double* wd = wf + (size_t)p * 4;
@@ -668,8 +673,9 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
       };
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
-        const int bb = h * BH + bl;
-        const int e0 = st[min(4 * bb, G)], e1 = st[min(4 * bb + 4, G)];
+        const int bb = SS ? bl : h * BH + bl;
+        const int e0 = SS ? max(st[min(4 * bb, G)], p_lo) : st[min(4 * bb, G)];
+        const int e1 = SS ? min(st[min(4 * bb + 4, G)], p_hi) : st[min(4 * bb + 4, G)];
         int kc = e0;
         for (; kc + 4 < e1; kc += 8) {  // two groups in flight
           double a0, a1;
@@ -718,7 +724,7 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
     if (h == hh) {
 #pragma unroll
       for (int bl = 0; bl < BH; ++bl) {
-        const int r = 4 * (h * BH + bl) + grp;
+        const int r = 4 * (SS ? bl : h * BH + bl) + grp;
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -922,11 +928,11 @@ static bool tc3_enabled() {
   return !off;
 }
 
-template <int RB, int NT, int FPB, int WPF>
+template <int RB, int NT, int FPB, int WPF, bool SS = false>
 static int tc3_launch(const CUtensorMap& map, const float* C, const float* scale, float* dC, float* dscale,
                       unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
                       cudaStream_t st, const int32_t* seg = nullptr) {
-  auto kern = kan_bwd_tc3_sweep_kernel<RB, NT, FPB, WPF>;
+  auto kern = kan_bwd_tc3_sweep_kernel<RB, NT, FPB, WPF, SS>;
   const size_t smem = tc3_smem(G, FPB, RB, NT);
   UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 gridd((d_out + 8 * NT - 1) / (8 * NT), (d_in + FPB - 1) / FPB, p.S);
@@ -1413,13 +1419,22 @@ int kan_bwd_tc_part(const float* C, const float* scale, const float* gy, float* 
 // inside the segment, UKAN u); table gradient: the tc3 sweep writing dT rows of the segment;
 // dx: kan_dx_tc_kernel staging C' from the segment.  Replaces the sorted-merge sweep
 // (seg_fsweep) and the per-pair dx (spline_dx64) for those layers, layers.py:254-291.
-static int ukan_dense_G(int64_t max_rows) { return (int)std::max<int64_t>(17, max_rows - 3); }
+// Segments of <= 16 rows (4 row blocks) take the sample-split sweep (SS), larger ones the
+// block-split tc3 sweep over >= 17 cells (two or four 4-block warps per feature).
+bool ukan_dense_ss(int64_t max_rows) {
+  static const bool off = getenv("UKAN_DENSE_SS") && getenv("UKAN_DENSE_SS")[0] == '0';  // A/B only
+  return !off && max_rows <= 16;
+}
+static int ukan_dense_G(int64_t max_rows) {
+  return ukan_dense_ss(max_rows) ? (int)std::max<int64_t>(1, max_rows - 3) : (int)std::max<int64_t>(17, max_rows - 3);
+}
 
 int64_t ukan_dense_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k) {
   static const bool off = getenv("UKAN_UKAN_DENSE") && getenv("UKAN_UKAN_DENSE")[0] == '0';  // A/B only
   if (off || k != 3 || B < 1 || max_rows < 1 || max_rows > 67 || d_out < 64 || d_out % 4 || !tc3_enabled()) return 0;
   const TcPlan p = kan_bwd_tc_plan(B, d_in, d_out, ukan_dense_G(max_rows), 3, false);
-  if (!p.ok || !p.split || p.wpf != 4) return 0;
+  if (!p.ok) return 0;
+  if (ukan_dense_ss(max_rows) ? p.rb != 4 : (!p.split || p.wpf != 4)) return 0;
   return kan_bwd_tc_workspace(p);  // records + split-K partials (padded [d_in][G+3] rows)
 }
 
@@ -1444,7 +1459,12 @@ int ukan_dense_backward(const float* x, const int32_t* base_row, const int32_t* 
     CUtensorMap map;
     if (!((uintptr_t)gy % 16 == 0 && tc3_tensor_map(&map, gy, B, d_out))) return UKAN_E_ARG;
     int rc = UKAN_E_ARG;
-    if (p.rb == 16 && p.nt == 4)
+    if (ukan_dense_ss(max_rows)) {
+      TcPlan q = p;  // one chunk range per CTA: the SS epilogue writes the rows directly
+      q.S = 1;
+      q.cps = q.nch;
+      rc = tc3_launch<4, 4, 4, 4, true>(map, T, scale, dT, dscale, recs, nullptr, B, d_in, d_out, G, q, st, seg);
+    } else if (p.rb == 16 && p.nt == 4)
       rc = tc3_launch<16, 4, 4, 4>(map, T, scale, dT, dscale, recs, part, B, d_in, d_out, G, p, st, seg);
     else if (p.rb == 8 && p.nt == 8)
       rc = tc3_launch<8, 8, 4, 4>(map, T, scale, dT, dscale, recs, part, B, d_in, d_out, G, p, st, seg);

@@ -1072,13 +1072,14 @@ extern "C" int64_t ukan_ukan_backward_workspace_size(int64_t B, int64_t d_in, in
   return (int64_t)sizeof(double) * n_u * (k + 1) * d_out;
 }
 
-// Dense UKAN layers: the table gradient on the banded DMMA sweep when the features' segments have
-// enough rows to keep its four warps per feature busy, else on the sorted-merge sweep (seg_*),
-// whose warps are not tied to row blocks (cfg5 layers with <= 12 rows: 13.7 vs 15.3 ms); dx
-// always on the DMMA dx.  A/B: UKAN_DENSE_SWEEP_MIN_ROWS.
+// Dense UKAN layers: the table gradient on the banded DMMA sweep — block-split when the features'
+// segments have >= 24 rows (enough blocks to keep four warps per feature busy), sample-split for
+// <= 16 rows — else on the sorted-merge sweep (seg_*); dx always on the DMMA dx.
+// A/B: UKAN_DENSE_SWEEP_MIN_ROWS, UKAN_DENSE_SS.
+namespace ukan { bool ukan_dense_ss(int64_t max_rows); }
 static bool ukan_dense_sweep(int64_t max_rows) {
   static const int64_t min_rows = getenv("UKAN_DENSE_SWEEP_MIN_ROWS") ? atoll(getenv("UKAN_DENSE_SWEEP_MIN_ROWS")) : 24;
-  return max_rows >= min_rows;
+  return ukan_dense_ss(max_rows) || max_rows >= min_rows;
 }
 
 extern "C" int64_t ukan_ukan_backward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
