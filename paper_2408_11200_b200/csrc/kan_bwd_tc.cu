@@ -609,7 +609,7 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
   if (producer) {
     for (int d = 0; d < kTc3Depth; ++d) {
       tc_mb_init(&full_s[d], 1);
-      tc_mb_init(&empty_s[d], NWARP);
+      tc_mb_init(&empty_s[d], NWARP * 32);  // every thread releases its own reads (release semantics per thread)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
@@ -705,9 +705,8 @@ kan_bwd_tc3_sweep_kernel(const __grid_constant__ CUtensorMap gmap, const unsigne
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) tc_mb_arrive(&empty_s[d]);
-    // refill this stage with chunk c+2 once every warp has released chunk c
+    tc_mb_arrive(&empty_s[d]);
+    // refill this stage with chunk c+2 once every thread has released chunk c
     if (producer && c + kTc3Depth < nchunk) {
       tc_mb_wait(&empty_s[d], (uint32_t)((c / kTc3Depth) & 1));
       issue(c + kTc3Depth);
