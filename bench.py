@@ -473,7 +473,8 @@ def cfg5_rate(dev, world, rank, steps=5, warmup=2):
     return {"workload": "cfg5: UKAN [64,512,512,64] k=3 delta_g=0.4 d_pe=d_femb=24, MSE + Adam, global batch 65536 "
                         f"sharded over {world} GPU(s) ({Bl} per GPU), NCCL all-reduce of the gradients",
             "samples_per_s": Bg / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "scaling": "strong",
-            "n_gpus": world, "path": "SplineTrainer.step (eager: one host read of the key count per UKAN layer)"}
+            "n_gpus": world, "path": "SplineTrainer.step (eager: one host read of the key count per UKAN layer); "
+                    "dense layers (<= 67 rows per feature) on the FP64 tensor-core backward"}
 
 
 def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
