@@ -99,7 +99,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             f"{path} is missing: build it with `python -m paper_2408_11200_b200.csrc.build` "
             "(the CUDA extension is required; there is no CPU fallback)")
     lib = ctypes.CDLL(path)
+    older_build = bool(os.environ.get("UKAN_B200_LIB"))  # A/B tooling may load an older build
     for name, (res, args) in SIGNATURES.items():
+        if older_build and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -1122,7 +1122,7 @@ __device__ __forceinline__ void dx_tile(const float* __restrict__ gb, const doub
   }
 }
 
-template <int kDxW, int MAXT>
+template <int kDxW, int MAXT, bool UK = false>  // UK: dense UKAN, each feature's rows = its table segment (seg)
 __global__ void __launch_bounds__(kDxW * 32, 1)
 kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict__ C, const float* __restrict__ scale,
                  const float* __restrict__ gy, float* __restrict__ dx, int B, int d_in, int d_out, int G, int nch,
@@ -1150,12 +1150,14 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
   const int i0 = fg * kDxF;
   const int b0 = n * kTcBC;
   const int nb = min(kTcBC, B - b0);
-  if (threadIdx.x < kDxF) {
-    const int ii = min(i0 + (int)threadIdx.x, d_in - 1);
-    rbase_s[threadIdx.x] = seg ? 4 * seg[ii] : ii * (G + 3);
-    nr_s[threadIdx.x] = seg ? 4 * (seg[ii + 1] - seg[ii]) : G + 3;
+  if constexpr (UK) {
+    if (threadIdx.x < kDxF) {
+      const int ii = min(i0 + (int)threadIdx.x, d_in - 1);
+      rbase_s[threadIdx.x] = 4 * seg[ii];
+      nr_s[threadIdx.x] = 4 * (seg[ii + 1] - seg[ii]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   unsigned char* rec_s = smem_raw + L.rec;
   int4* task_s = reinterpret_cast<int4*>(smem_raw + L.task);
   float* g_s = reinterpret_cast<float*>(smem_raw + L.g);
@@ -1192,8 +1194,13 @@ kan_dx_tc_kernel(const unsigned char* __restrict__ recs, const float* __restrict
       const int t = threadIdx.x + q * kDxW * 32;
       const int j = (t % nq) * 4, fr = t / nq, r = fr % RR, f = fr / RR;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (f < kDxF && i0 + f < d_in && r < nr_s[f] && o0 + j < d_out)
-        v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)rbase_s[f] + r) * d_out + o0 + j));
+      if constexpr (UK) {
+        if (f < kDxF && i0 + f < d_in && r < nr_s[f] && o0 + j < d_out)
+          v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)rbase_s[f] + r) * d_out + o0 + j));
+      } else {
+        if (f < kDxF && r < R && i0 + f < d_in && o0 + j < d_out)
+          v = __ldg(reinterpret_cast<const float4*>(C + ((size_t)(i0 + f) * R + r) * d_out + o0 + j));
+      }
       cr[q] = v;
     }
   };
@@ -1353,7 +1360,12 @@ static int dx_tc_launch(const float* C, const float* scale, const float* gy, flo
   static const int warps_env = getenv("UKAN_DX_WARPS") ? atoi(getenv("UKAN_DX_WARPS")) : 16;
   const int band = std::max(1, std::min(band_env, nch));
   const int64_t nblk = (int64_t)nch * n_fg;
-  if (warps_env == 16) {
+  if (seg != nullptr) {
+    auto kern = kan_dx_tc_kernel<16, 12, true>;
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    kern<<<(unsigned)nblk, 16 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
+                                                   grid.inv_dg, make_basis<4>(3), seg);
+  } else if (warps_env == 16) {
     auto kern = kan_dx_tc_kernel<16, 12>;
     UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<(unsigned)nblk, 16 * 32, L.total, st>>>(recs, C, scale, gy, dx, B, d_in, d_out, G, nch, n_fg, band, ld,
