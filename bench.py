@@ -384,6 +384,13 @@ def our_arm(args, rank, world, local_rank):
                          "unit": "GB/s", "frac": hbm / (ms_max / args.steps * 1e-3) / 1e9 / pk["hbm_gbs"],
                          "note": "compulsory bytes of the whole layer step (SURVEY 8d D2); the step is compute-bound "
                                  "(FP32 forward, FP64 backward forced by the parity bar)"},
+        "roofline_phases": {  # every phase of the step against its own pipe (useful flops: 2*K*B*d_in*d_out)
+            ph: {"kernel": phase_info[ph][0], "ms": phase_ms[ph], "achieved_tflops": f_pass / (phase_ms[ph] * 1e-3) / 1e12,
+                 "peak_tflops": phase_info[ph][1],
+                 "frac": f_pass / (phase_ms[ph] * 1e-3) / 1e12 / phase_info[ph][1],
+                 "frac_of_banded_ceiling": (f_pass / (phase_ms[ph] * 1e-3) / 1e12 / (0.5 * phase_info[ph][1])
+                                            if "DMMA" in phase_info[ph][2] else None)}
+            for ph in phase_info if ph in phase_ms},
         "step_tflops": step_tflops,
         "roof_ms": (f_pass / (FP32_TFLOPS_MEASURED * 1e12) + 2 * f_pass / (FP64_TFLOPS_MEASURED * 1e12)) * 1e3,
         "phase_ms": phase_ms,

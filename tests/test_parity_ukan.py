@@ -176,7 +176,7 @@ def test_ukan_segmented_sweep_multi_chunk(d_out, sigma):
 
 
 @pytest.mark.parametrize("B,d_in,d_out,dg,sigma", [(1500, 12, 64, 0.4, 1.0), (700, 9, 100, 1.0, 7.0), (257, 33, 256, 0.5, 2.0),
-                                                  (2000, 16, 64, 0.4, 0.3)])
+                                                  (2000, 16, 64, 0.4, 0.3), (1, 5, 64, 0.4, 1.0), (5, 7, 68, 0.4, 1.0)])
 def test_ukan_dense_layer_on_tensor_cores(B, d_in, d_out, dg, sigma):
     """Dense UKAN layers (every feature's virtual table <= 67 rows, the cfg5 regime) take the KAN
     FP64 tensor-core backward (ukan_ukan_backward_dense): multi-chunk, ragged output tiles
