@@ -251,6 +251,14 @@ int ukan_ukan_backward(const float* x, const int32_t* base_row, const int32_t* s
                        double delta_g, void* workspace, int64_t workspace_bytes,
                        void* stream);
 
+/* Dense UKAN forward (max_rows <= 67, k = 3, d_out >= 128): ukan_ukan_forward's result through the
+ * TMEM-gather forward over the features' table segments.  Size 0 = the layer does not qualify. */
+int64_t ukan_ukan_forward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k);
+int ukan_ukan_forward_dense(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                            const float* table, const float* scale, float* y, int64_t B, int64_t d_in,
+                            int64_t d_out, int64_t max_rows, int k, double delta_g, void* workspace,
+                            int64_t workspace_bytes, void* stream);
+
 /* Dense UKAN layers (every feature's virtual table has max_rows <= 67 rows, k = 3, d_out >= 64,
  * d_out % 4 == 0): the same gradients as ukan_ukan_backward (layers.py:254-291 backward) on the
  * KAN FP64 tensor-core backward — cell-sorted records per (feature, 256-sample chunk), the banded

@@ -125,8 +125,11 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
 // Coefficient pack (once per forward): Cp[ot][i][r][256] = scale[i,o] * C[i,r,o], zero for
 // r >= R or o >= d_out.  Each (o-tile, feature) slab is then one contiguous RP KB block, so a
 // stage is a single 1-D TMA bulk copy, and each lane's 16 bytes of a row are contiguous.
+// seg != nullptr (dense UKAN layer): feature i's R rows are rows [4 seg[i], 4 seg[i+1]) of the
+// generated table (zero past the segment) instead of C[i].
 __global__ void kan_pack_coeffs_kernel(const float* __restrict__ C, const float* __restrict__ scale,
-                                       float4* __restrict__ Cp, int d_in, int R, int RP, int d_out, int n_ot) {
+                                       float4* __restrict__ Cp, int d_in, int R, int RP, int d_out, int n_ot,
+                                       const int32_t* __restrict__ seg = nullptr) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)n_ot * d_in * RP * (kTmOT / 4);
   if (t >= n) return;
@@ -137,10 +140,11 @@ __global__ void kan_pack_coeffs_kernel(const float* __restrict__ C, const float*
   const int i = (int)(rest % d_in);
   const int ot = (int)(rest / d_in);
   float v[4];
+  const int rbase = seg ? 4 * seg[i] : i * R, nr = seg ? 4 * (seg[i + 1] - seg[i]) : R;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int o = ot * kTmOT + q * 4 + e;
-    v[e] = (r < R && o < d_out) ? C[((size_t)i * R + r) * d_out + o] * scale[(size_t)i * d_out + o] : 0.f;
+    v[e] = (r < nr && o < d_out) ? C[((size_t)rbase + r) * d_out + o] * scale[(size_t)i * d_out + o] : 0.f;
   }
   Cp[t] = make_float4(v[0], v[1], v[2], v[3]);
 }
@@ -149,10 +153,13 @@ __global__ void kan_pack_coeffs_kernel(const float* __restrict__ C, const float*
 //   cell[i][b] (u8) and w[i][b][KP] (fp32, from the fp64 basis) — fp64 locate with the
 //   reference's expression order (layers.py:299-300).  NaN input sets *err (the reference
 //   raises IndexError, SURVEY gotcha 10) and contributes nothing.
-template <int K>
+// UK (dense UKAN layer): the cell is the window start inside the feature's table segment,
+// base_row[b, i] - 4 seg[i], and u = x/dg - floor(x/dg) (layers.py:261-264).
+template <int K, bool UK = false>
 __global__ void __launch_bounds__(256)
 kan_fwd_records_kernel(const float* __restrict__ x, uint8_t* __restrict__ cell_out, float* __restrict__ w_out, int B,
-                       int Bp, int d_in, KanGrid grid, Basis<K> bas, int32_t* __restrict__ err) {
+                       int Bp, int d_in, KanGrid grid, Basis<K> bas, int32_t* __restrict__ err,
+                       const int32_t* __restrict__ base_row = nullptr, const int32_t* __restrict__ seg = nullptr) {
   constexpr int KP = (K + 3) / 4 * 4;
   __shared__ float xs[32][33];  // 32 samples x 32 features, transposed through shared memory
   const int b0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
@@ -171,7 +178,16 @@ kan_fwd_records_kernel(const float* __restrict__ x, uint8_t* __restrict__ cell_o
     for (int j = 0; j < KP; ++j) wf[j] = 0.f;
     double u;
     bool mask;
-    if (kan_locate(xs[tx][r], grid, cell, u, mask)) {
+    bool ok;
+    if constexpr (UK) {
+      int64_t gid;
+      ukan_locate(xs[tx][r], grid.inv_dg, gid, u);
+      cell = base_row[(size_t)b * d_in + i] - 4 * seg[i];
+      ok = cell >= 0 && cell < grid.G && u == u;
+    } else {
+      ok = kan_locate(xs[tx][r], grid, cell, u, mask);
+    }
+    if (ok) {
       double w[K];
       basis_weights<K>(bas, u, w);
 #pragma unroll
@@ -437,7 +453,8 @@ int64_t kan_fwd_tm_workspace(const TmPlan& p) {
 
 template <int K>
 static int launch_tm(const float* x, const float* C, const float* scale, float* y, void* ws, int B, int d_in,
-                     int d_out, int R, const KanGrid& grid, const TmPlan& p, int32_t* err, cudaStream_t st) {
+                     int d_out, int R, const KanGrid& grid, const TmPlan& p, int32_t* err, cudaStream_t st,
+                     const int32_t* base_row = nullptr, const int32_t* seg = nullptr) {
   constexpr int SW = kTmST / (2 * kTmWarpsQ);
   constexpr int KP = (K + 3) / 4 * 4;
   char* w8 = static_cast<char*>(ws);
@@ -447,11 +464,17 @@ static int launch_tm(const float* x, const float* C, const float* scale, float* 
   float* part = reinterpret_cast<float*>(w8 + al256(p.pack_bytes) + al256(p.rec_bytes));
   const int64_t npack = (int64_t)p.n_ot * d_in * p.RP * (kTmOT / 4);
   kan_pack_coeffs_kernel<<<(unsigned)((npack + 255) / 256), 256, 0, st>>>(C, scale, reinterpret_cast<float4*>(Cp),
-                                                                         d_in, R, p.RP, d_out, p.n_ot);
+                                                                         d_in, R, p.RP, d_out, p.n_ot, seg);
   UKAN_LAUNCH_CHECK();
   if (p.Bp > B) UKAN_CUDA_TRY(cudaMemsetAsync(recw, 0, p.rec_bytes, st));  // padding samples: zero weights
-  kan_fwd_records_kernel<K><<<dim3((B + 31) / 32, (d_in + 31) / 32), 256, 0, st>>>(x, recc, recw, B, p.Bp, d_in, grid,
-                                                                                   make_basis<K>(K - 1), err);
+  if (seg != nullptr) {
+    if constexpr (K == 4)
+      kan_fwd_records_kernel<K, true><<<dim3((B + 31) / 32, (d_in + 31) / 32), 256, 0, st>>>(
+          x, recc, recw, B, p.Bp, d_in, grid, make_basis<K>(K - 1), err, base_row, seg);
+  } else {
+    kan_fwd_records_kernel<K><<<dim3((B + 31) / 32, (d_in + 31) / 32), 256, 0, st>>>(x, recc, recw, B, p.Bp, d_in,
+                                                                                     grid, make_basis<K>(K - 1), err);
+  }
   UKAN_LAUNCH_CHECK();
   auto kern = p.depth == kTmSDepth ? (p.db ? kan_fwd_tm_kernel<K, SW, kTmSDepth, true> : kan_fwd_tm_kernel<K, SW, kTmSDepth, false>)
                                     : (p.db ? kan_fwd_tm_kernel<K, SW, 3, true> : kan_fwd_tm_kernel<K, SW, 3, false>);
@@ -474,6 +497,18 @@ int kan_fwd_tm_run(const float* x, const float* C, const float* scale, float* y,
   if (!p.ok || ws == nullptr || ws_bytes < kan_fwd_tm_workspace(p)) return UKAN_E_WORKSPACE;
   if constexpr (K <= 8) return launch_tm<K>(x, C, scale, y, ws, B, d_in, d_out, R, grid, p, err, st);
   return UKAN_E_ARG;
+}
+
+// Dense UKAN layer (every feature's table segment <= G + 3 rows): the same TMEM forward over the
+// segments of the generated table (cubic only).
+int kan_fwd_tm_run_ukan(const float* x, const float* T, const float* scale, float* y, void* ws, int64_t ws_bytes,
+                        int B, int d_in, int d_out, int G, double inv_dg, const int32_t* base_row, const int32_t* seg,
+                        const TmPlan& p, cudaStream_t st) {
+  if (!p.ok || ws == nullptr || ws_bytes < kan_fwd_tm_workspace(p)) return UKAN_E_WORKSPACE;
+  KanGrid grid{};
+  grid.inv_dg = inv_dg;
+  grid.G = G;
+  return launch_tm<4>(x, T, scale, y, ws, B, d_in, d_out, G + 3, grid, p, nullptr, st, base_row, seg);
 }
 
 #define UKAN_TM_INST(K)                                                                                          \

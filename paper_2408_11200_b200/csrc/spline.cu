@@ -571,6 +571,9 @@ int kan_small_tablegrad(const float* x, const float* C, const float* scale, cons
                         void* ws, int B, int d_in, int d_out, int G, const KanGrid& grid, bool prepared,
                         cudaStream_t st);
 int64_t kan_fwd_tm_workspace(const TmPlan& p);
+int kan_fwd_tm_run_ukan(const float* x, const float* T, const float* scale, float* y, void* ws, int64_t ws_bytes,
+                        int B, int d_in, int d_out, int G, double inv_dg, const int32_t* base_row, const int32_t* seg,
+                        const TmPlan& p, cudaStream_t st);
 template <int K>
 int kan_fwd_tm_run(const float* x, const float* C, const float* scale, float* y, void* ws, int64_t ws_bytes, int B,
                    int d_in, int d_out, int R, const KanGrid& grid, const TmPlan& p, int32_t* err, cudaStream_t st);
@@ -1053,6 +1056,34 @@ extern "C" int ukan_ukan_forward(const float* x, const int32_t* base_row, const 
   cudaStream_t st = (cudaStream_t)stream;
   UKAN_DISPATCH_K(k, return launch_fwd<K, true>(x, table, scale, nullptr, y, (int)B, (int)d_in, (int)d_out, rm, nullptr, st););
   return UKAN_OK;
+}
+
+// Dense UKAN forward: the TMEM-gather forward over the features' table segments (max_rows from the
+// key build <= 67, cubic, d_out >= 128); size 0 when the layer does not qualify.
+static TmPlan ukan_dense_fwd_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k) {
+  static const bool off = getenv("UKAN_UKAN_DENSE") && getenv("UKAN_UKAN_DENSE")[0] == '0';  // A/B only
+  if (off || k != 3 || B < 1 || max_rows < 4 || max_rows > 67 || !fwd_use_tm()) return TmPlan{};
+  return kan_fwd_tm_plan(B, d_in, d_out, max_rows - 3, 3, false);
+}
+
+extern "C" int64_t ukan_ukan_forward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows,
+                                                         int k) {
+  if (B > INT32_MAX || d_in < 1 || d_out < 1) return 0;
+  return kan_fwd_tm_workspace(ukan_dense_fwd_plan(B, d_in, d_out, max_rows, k));
+}
+
+extern "C" int ukan_ukan_forward_dense(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                                       const float* table, const float* scale, float* y, int64_t B, int64_t d_in,
+                                       int64_t d_out, int64_t max_rows, int k, double delta_g, void* workspace,
+                                       int64_t workspace_bytes, void* stream) {
+  if (k != 3) return UKAN_E_DEGREE;
+  if (!(delta_g > 0)) return UKAN_E_GRID;
+  if (!x || !base_row || !seg_start || !table || !scale || !y || B < 1 || d_in < 1 || d_out < 1 || B > INT32_MAX)
+    return UKAN_E_ARG;
+  const TmPlan tp = ukan_dense_fwd_plan(B, d_in, d_out, max_rows, k);
+  if (!tp.ok) return UKAN_E_ARG;
+  return kan_fwd_tm_run_ukan(x, table, scale, y, workspace, workspace_bytes, (int)B, (int)d_in, (int)d_out,
+                             (int)max_rows - 3, 1.0 / delta_g, base_row, seg_start, tp, (cudaStream_t)stream);
 }
 
 // Sorted-chunk segmented sweep (kan_bwd_wide.cu) when the per-feature local row index fits the

@@ -299,8 +299,7 @@ class UkanSplineFn(torch.autograd.Function):
         B, d_in = x.shape
         d_out = scale.shape[1]
         y = torch.empty((B, d_out), device=x.device, dtype=torch.float32)
-        check(lib.ukan_ukan_forward(ptr(x), ptr(base_row), ptr(table), ptr(scale), ptr(y), B, d_in, d_out, k,
-                                    delta_g, stream_ptr()), "ukan_forward")
+        ukan_forward_into(x, base_row, seg_start, table, scale, y, k, delta_g, max_rows)
         ctx.save_for_backward(x, table, scale, base_row, seg_start)
         ctx.meta = (k, float(delta_g), int(max_rows))
         return y
@@ -315,6 +314,24 @@ class UkanSplineFn(torch.autograd.Function):
         ds = torch.empty_like(scale)
         ukan_backward_into(x, base_row, seg_start, table, scale, gy, dx, dtable, ds, k, delta_g, max_rows)
         return dx, dtable, ds, None, None, None, None, None
+
+
+def ukan_forward_into(x, base_row, seg_start, table, scale, y, k: int, delta_g: float, max_rows: int = 0) -> None:
+    """y of the UKAN spline over the generated table (layers.py:284-291).  Dense layers (every
+    feature's segment <= 67 rows, d_out >= 128) take the TMEM-gather forward
+    (ukan_ukan_forward_dense); the others the gather kernel (ukan_ukan_forward)."""
+    lib = _lib.load()
+    B, d_in = x.shape
+    d_out = scale.shape[1]
+    st = stream_ptr()
+    nbytes = lib.ukan_ukan_forward_dense_workspace_size(B, d_in, d_out, max_rows, k) if max_rows > 0 else 0
+    if nbytes > 0:
+        ws = torch.empty(nbytes, device=x.device, dtype=torch.uint8)
+        check(lib.ukan_ukan_forward_dense(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(y), B,
+                                          d_in, d_out, max_rows, k, delta_g, ptr(ws), nbytes, st), "ukan_forward_dense")
+        return
+    check(lib.ukan_ukan_forward(ptr(x), ptr(base_row), ptr(table), ptr(scale), ptr(y), B, d_in, d_out, k, delta_g, st),
+          "ukan_forward")
 
 
 def ukan_backward_into(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, k: int, delta_g: float,

@@ -149,8 +149,8 @@ class SplineTrainer:
         self.kernel_launches += 5
         table, cg_cache = ops.cg_forward_raw(keys.key_f, keys.key_g, layer.feature_embedding, layer.cg_w1,
                                              layer.cg_b1, layer.cg_w2, layer.cg_b2, layer.d_pe)
-        check(self.lib.ukan_ukan_forward(ptr(h), ptr(keys.base_row), ptr(table), ptr(layer.scale), ptr(y), B,
-                                         layer.d_in, layer.d_out, layer.k, float(layer.delta_g), st), "ukan_forward")
+        ops.ukan_forward_into(h, keys.base_row, keys.seg_start, table, layer.scale, y, layer.k, float(layer.delta_g),
+                              keys.max_rows)
         self.kernel_launches += 4
         return y, (keys, cg_cache, table)
 

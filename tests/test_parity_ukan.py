@@ -176,17 +176,21 @@ def test_ukan_segmented_sweep_multi_chunk(d_out, sigma):
 
 
 @pytest.mark.parametrize("B,d_in,d_out,dg,sigma", [(1500, 12, 64, 0.4, 1.0), (700, 9, 100, 1.0, 7.0), (257, 33, 256, 0.5, 2.0),
-                                                  (2000, 16, 64, 0.4, 0.3), (1, 5, 64, 0.4, 1.0), (5, 7, 68, 0.4, 1.0)])
+                                                  (2000, 16, 64, 0.4, 0.3), (1, 5, 64, 0.4, 1.0), (5, 7, 68, 0.4, 1.0),
+                                                  (300, 6, 128, 0.4, 1.0)])
 def test_ukan_dense_layer_on_tensor_cores(B, d_in, d_out, dg, sigma):
     """Dense UKAN layers (every feature's virtual table <= 67 rows, the cfg5 regime) take the KAN
     FP64 tensor-core backward (ukan_ukan_backward_dense): multi-chunk, ragged output tiles
-    (d_out = 100), 8- and 16-row-block plans, few-row segments (sorted-merge table sweep + DMMA
-    dx); oracle parity and bitwise determinism."""
+    (d_out = 100), 8- and 16-row-block plans, few-row segments (sample-split sweep), and for
+    d_out >= 128 the TMEM-gather forward over the segments; oracle parity and bitwise determinism."""
     from paper_2408_11200_b200 import _lib
     layer, x, gup = random_case(B, d_in, d_out, 3, dg, 8, 8, seed=B + d_out, sigma=sigma)
     keys = ops.ukan_build_keys(_t(x), 3, dg)
     assert 0 < keys.max_rows <= 67
-    assert _lib.load().ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, keys.n_u, keys.max_rows, 3) > 0
+    lib = _lib.load()
+    assert lib.ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, keys.n_u, keys.max_rows, 3) > 0
+    if d_out >= 128 and keys.max_rows >= 4:  # the TMEM-gather forward over the segments too
+        assert lib.ukan_ukan_forward_dense_workspace_size(B, d_in, d_out, keys.max_rows, 3) > 0
     check_against_oracle(layer, x, gup)
     for p in layer.parameters().values():
         p.grad = None
