@@ -481,7 +481,7 @@ def cfg5_rate(dev, world, rank, steps=5, warmup=2):
                         f"sharded over {world} GPU(s) ({Bl} per GPU), NCCL all-reduce of the gradients",
             "samples_per_s": Bg / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "scaling": "strong",
             "n_gpus": world, "path": "SplineTrainer.step (eager: one host read of the key count per UKAN layer); "
-                    "dense layers (<= 67 rows per feature) on the FP64 tensor-core backward"}
+                    "dense layers (<= 67 rows per feature) on the FP64 tensor-core backward and the TMEM-gather forward"}
 
 
 def ukan_layer_rate(dev, B=4096, steps=5, warmup=3):
