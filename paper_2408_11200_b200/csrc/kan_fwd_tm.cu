@@ -216,7 +216,11 @@ constexpr int kTmSDepth = 5;  // shared-memory ring: TMA loads run up to 3 stage
 // DEPTH: shared-memory ring depth (5, or 3 when the slabs of finer grids do not fit five times);
 // DB: two TMEM slab buffers (the next feature's fill overlaps this feature's gathers) when two
 // slabs of RP x 4 columns fit the 512 TMEM columns, else one buffer refilled after a barrier.
-template <int K, int SW, int DEPTH, bool DB>
+// MC: a cluster of two CTAs (adjacent sample tiles of one output tile) shares each coefficient
+// slab: each CTA streams half of it with a multicast bulk copy into both CTAs' rings (half the
+// L2 -> SM slab traffic); a stage is refilled once the consumers of BOTH CTAs released it (every
+// warp arrives on its own and the peer's `empty` barrier).
+template <int K, int SW, int DEPTH, bool DB, bool MC = false>
 __global__ void __launch_bounds__(kTmThreads, 1)
 kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, const float* __restrict__ rw,
                   float* __restrict__ y, int B, int Bp, int d_in, int d_out, int RP, int fpc) {
@@ -248,10 +252,12 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
         (uint32_t)__cvta_generic_to_shared(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
+  uint32_t crank = 0;
+  if constexpr (MC) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
   if (producer) {
     for (int d = 0; d < DEPTH; ++d) {
       mb_init(&full_s[d], 1);
-      mb_init(&empty_s[d], NWARP);
+      mb_init(&empty_s[d], MC ? 2 * NWARP : NWARP);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -262,7 +268,17 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     const int i = i_lo + g;
     uint64_t* mb = &full_s[g % DEPTH];
     mb_expect_tx(mb, buf_bytes);
-    bulk_g2s(d, cp_ot + (size_t)i * RP * kTmOT, slab_bytes, mb);
+    if constexpr (MC) {  // this CTA's half of the slab, into both CTAs (same offsets, same barrier)
+      const uint32_t half = slab_bytes / 2;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+              (uint32_t)__cvta_generic_to_shared(d + crank * half)),
+          "l"(reinterpret_cast<const unsigned char*>(cp_ot + (size_t)i * RP * kTmOT) + crank * half), "r"(half),
+          "r"((uint32_t)__cvta_generic_to_shared(mb)), "h"((unsigned short)3)
+          : "memory");
+    } else {
+      bulk_g2s(d, cp_ot + (size_t)i * RP * kTmOT, slab_bytes, mb);
+    }
     bulk_g2s(d + slab_bytes, rw + ((size_t)i * Bp + b0) * KP, recw_bytes, mb);
     bulk_g2s(d + slab_bytes + recw_bytes, rc + (size_t)i * Bp + b0, kTmST, mb);
   };
@@ -282,7 +298,11 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     for (int v = 0; v < OV / 2; ++v) acc2[s][v] = make_float2(0.f, 0.f);
 
   tm_fence_before();
-  __syncthreads();  // TMEM address + mbarrier init visible
+  if constexpr (MC) {  // both CTAs' barriers initialised before any multicast / remote arrive
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    __syncthreads();  // TMEM address + mbarrier init visible
+  }
   tm_fence_after();
   const uint32_t tbase = tmem_base_s;
   const uint32_t tl = tbase + ((uint32_t)(32 * q) << 16);
@@ -349,9 +369,15 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
       }
     }
     __syncwarp();
-    if (lane == 0)  // done with stage g's shared buffer (slab copied into TMEM, records read)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((uint32_t)__cvta_generic_to_shared(&empty_s[ds]))
-                   : "memory");
+    if (lane == 0) {  // done with stage g's shared buffer (slab copied into TMEM, records read)
+      const uint32_t ea = (uint32_t)__cvta_generic_to_shared(&empty_s[ds]);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(ea) : "memory");
+      if constexpr (MC) {  // ... and the peer's: its next multicast into this CTA's buffer waits on it
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(ea), "r"(crank ^ 1u));
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra) : "memory");
+      }
+    }
     tm_wait_st();
     tm_fence_before();
     asm volatile("bar.sync %0, %1;\n" ::"r"(qbar), "r"(kTmWarpsQ * 32) : "memory");
@@ -384,7 +410,11 @@ kan_fwd_tm_kernel(const float* __restrict__ Cp, const uint8_t* __restrict__ rc, 
     }
   }
   tm_fence_before();
-  __syncthreads();
+  if constexpr (MC) {  // the peer may still arrive on this CTA's barriers until it is done
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   tm_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
@@ -432,7 +462,7 @@ TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   p.smem = (size_t)p.depth * per;
   if (p.smem > 220 * 1024) return p;
   p.n_ot = (int)((d_out + kTmOT - 1) / kTmOT);
-  p.Bp = (int)((B + kTmST - 1) / kTmST * kTmST);
+  p.Bp = (int)((B + 2 * kTmST - 1) / (2 * kTmST) * (2 * kTmST));  // even tile count: cluster pairs (MC)
   const int64_t tiles = (p.Bp / kTmST) * (int64_t)p.n_ot;
   const int sms = kan_num_sms();
   int64_t S = 1;  // split d_in so the grid fills the SMs without a partial second wave
@@ -476,12 +506,34 @@ static int launch_tm(const float* x, const float* C, const float* scale, float* 
                                                                                      grid, make_basis<K>(K - 1), err);
   }
   UKAN_LAUNCH_CHECK();
-  auto kern = p.depth == kTmSDepth ? (p.db ? kan_fwd_tm_kernel<K, SW, kTmSDepth, true> : kan_fwd_tm_kernel<K, SW, kTmSDepth, false>)
-                                    : (p.db ? kan_fwd_tm_kernel<K, SW, 3, true> : kan_fwd_tm_kernel<K, SW, 3, false>);
-  UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   dim3 gridd(p.Bp / kTmST, p.n_ot, p.S);
   float* out = p.S > 1 ? part : y;
-  kern<<<gridd, kTmThreads, p.smem, st>>>(Cp, recc, recw, out, B, p.Bp, d_in, d_out, p.RP, p.fpc);
+  static const bool mc = getenv("UKAN_FWD_MC") && getenv("UKAN_FWD_MC")[0] == '1';  // A/B
+  if (mc) {
+    auto kern = p.depth == kTmSDepth
+                    ? (p.db ? kan_fwd_tm_kernel<K, SW, kTmSDepth, true, true> : kan_fwd_tm_kernel<K, SW, kTmSDepth, false, true>)
+                    : (p.db ? kan_fwd_tm_kernel<K, SW, 3, true, true> : kan_fwd_tm_kernel<K, SW, 3, false, true>);
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = gridd;
+    cfg.blockDim = dim3(kTmThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    UKAN_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const float*)Cp, (const uint8_t*)recc, (const float*)recw, out, B,
+                                     p.Bp, d_in, d_out, p.RP, p.fpc));
+  } else {
+    auto kern = p.depth == kTmSDepth ? (p.db ? kan_fwd_tm_kernel<K, SW, kTmSDepth, true> : kan_fwd_tm_kernel<K, SW, kTmSDepth, false>)
+                                      : (p.db ? kan_fwd_tm_kernel<K, SW, 3, true> : kan_fwd_tm_kernel<K, SW, 3, false>);
+    UKAN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    kern<<<gridd, kTmThreads, p.smem, st>>>(Cp, recc, recw, out, B, p.Bp, d_in, d_out, p.RP, p.fpc);
+  }
   UKAN_LAUNCH_CHECK();
   if (p.S > 1) {
     const int64_t n = (int64_t)B * d_out;
