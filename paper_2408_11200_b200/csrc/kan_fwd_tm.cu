@@ -462,7 +462,9 @@ TmPlan kan_fwd_tm_plan(int64_t B, int64_t d_in, int64_t d_out, int64_t G, int k,
   p.smem = (size_t)p.depth * per;
   if (p.smem > 220 * 1024) return p;
   p.n_ot = (int)((d_out + kTmOT - 1) / kTmOT);
-  p.Bp = (int)((B + 2 * kTmST - 1) / (2 * kTmST) * (2 * kTmST));  // even tile count: cluster pairs (MC)
+  static const bool mc = getenv("UKAN_FWD_MC") && getenv("UKAN_FWD_MC")[0] == '1';  // cluster pairs: even tile count
+  const int tile = mc ? 2 * kTmST : kTmST;
+  p.Bp = (int)((B + tile - 1) / tile * tile);
   const int64_t tiles = (p.Bp / kTmST) * (int64_t)p.n_ot;
   const int sms = kan_num_sms();
   int64_t S = 1;  // split d_in so the grid fills the SMs without a partial second wave
