@@ -251,6 +251,17 @@ int ukan_ukan_backward(const float* x, const int32_t* base_row, const int32_t* s
                        double delta_g, void* workspace, int64_t workspace_bytes,
                        void* stream);
 
+/* ukan_ukan_backward with the key build's *max_rows_host: dense layers take
+ * ukan_ukan_backward_dense, the others the sorted-merge path with max_rows bounding the per-feature
+ * row histogram (which admits large batches to the per-feature sorted sweep). */
+int64_t ukan_ukan_backward2_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
+                                           int64_t max_rows, int k);
+int ukan_ukan_backward2(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                        const float* table, const float* scale, const float* gy,
+                        float* dx, float* dtable, float* dscale,
+                        int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int64_t max_rows, int k,
+                        double delta_g, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Dense UKAN forward (max_rows <= 67, k = 3, d_out >= 128): ukan_ukan_forward's result through the
  * TMEM-gather forward over the features' table segments.  Size 0 = the layer does not qualify. */
 int64_t ukan_ukan_forward_dense_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t max_rows, int k);

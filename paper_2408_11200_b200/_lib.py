@@ -76,6 +76,9 @@ SIGNATURES: dict[str, tuple] = {
     "ukan_ukan_backward_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),
     "ukan_ukan_forward_dense_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _INT]),
     "ukan_ukan_forward_dense": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _F64, _P, _I64, _P]),
+    "ukan_ukan_backward2_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _I64, _INT]),
+    "ukan_ukan_backward2": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _INT, _F64, _P,
+                                   _I64, _P]),
     "ukan_ukan_backward_dense_workspace_size": (_I64, [_I64, _I64, _I64, _I64, _I64, _INT]),
     "ukan_ukan_backward_dense": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _INT, _F64,
                                         _P, _I64, _P]),

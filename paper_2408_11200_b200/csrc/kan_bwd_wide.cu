@@ -1005,10 +1005,13 @@ int64_t seg_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t total_rows
   return rec + ts + ((int64_t)sizeof(double) * tiles * d_out + 255) / 256 * 256 + sorted;
 }
 
+// max_rows_hint > 0: the largest per-feature row count (the key build reports it); without it the
+// bound 2*B*K keeps large batches off the per-feature sorted sweep (its row histogram lives in
+// shared memory) although the real segments are a few hundred rows.
 template <int K, bool UKAN>
 int seg_table_grad(const float* x, const float* T, const float* scale, const float* gy, float* dT, float* dscale,
                    void* ws, int64_t ws_bytes, int B, int d_in, int d_out, int64_t total_rows, const RowMap& rm,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t max_rows_hint) {
   if (ws == nullptr || ws_bytes < seg_workspace(B, d_in, d_out, total_rows)) return UKAN_E_WORKSPACE;
   const int nch = (B + kWdBC - 1) / kWdBC;
   unsigned char* recs = reinterpret_cast<unsigned char*>(ws);
@@ -1022,7 +1025,8 @@ int seg_table_grad(const float* x, const float* T, const float* scale, const flo
   UKAN_LAUNCH_CHECK();
   static const bool cuda_cores = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == '1';  // A/B only
   static const bool tiles_only = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == 't';  // A/B only
-  const int64_t max_rows = std::min<int64_t>(total_rows, 2 * (int64_t)B * K);
+  int64_t max_rows = std::min<int64_t>(total_rows, 2 * (int64_t)B * K);
+  if (max_rows_hint > 0) max_rows = std::min<int64_t>(max_rows, max_rows_hint);
   if constexpr (K == 4) {
     if (!cuda_cores && !tiles_only && max_rows + 1 <= kFsMaxRows) {
       unsigned char* base = recs + rec + ((4 * ((int64_t)d_in + 1) + 255) / 256) * 256 +
@@ -1072,7 +1076,7 @@ int seg_table_grad(const float* x, const float* T, const float* scale, const flo
 
 #define UKAN_SEG_INST(K)                                                                                        \
   template int seg_table_grad<K, true>(const float*, const float*, const float*, const float*, float*, float*, \
-                                       void*, int64_t, int, int, int, int64_t, const RowMap&, cudaStream_t);
+                                       void*, int64_t, int, int, int, int64_t, const RowMap&, cudaStream_t, int64_t);
 UKAN_SEG_INST(1) UKAN_SEG_INST(2) UKAN_SEG_INST(3) UKAN_SEG_INST(4) UKAN_SEG_INST(5) UKAN_SEG_INST(6)
 UKAN_SEG_INST(7) UKAN_SEG_INST(8) UKAN_SEG_INST(9) UKAN_SEG_INST(10) UKAN_SEG_INST(11)
 

@@ -600,7 +600,8 @@ bool seg_supported(int64_t B, int64_t d_out);
 template <int K, bool UKAN>
 int seg_table_grad(const float* x, const float* T, const float* scale, const float* gy, float* dT, float* dscale,
                    void* ws, int64_t ws_bytes, int B, int d_in, int d_out, int64_t total_rows, const RowMap& rm,
-                   cudaStream_t st);
+                   cudaStream_t st,
+                   int64_t max_rows_hint = 0);
 template <int K>
 int kan_fwd_v2(const float* x, const float* C, const float* scale, const float* bw, float* y, int B, int d_in,
                int d_out, int R, const KanGrid& grid, int32_t* err, cudaStream_t st);
@@ -1153,12 +1154,11 @@ extern "C" int ukan_ukan_backward_dense(const float* x, const int32_t* base_row,
                              (int)d_out, max_rows, delta_g, workspace, tc, st, sweep);
 }
 
-extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
-                                  const int32_t* seg_start, const float* table,
-                                  const float* scale, const float* gy, float* dx, float* dtable,
-                                  float* dscale, int64_t B, int64_t d_in, int64_t d_out,
-                                  int64_t n_u, int k, double delta_g, void* workspace,
-                                  int64_t workspace_bytes, void* stream) {
+static int ukan_backward_impl(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                              const float* table, const float* scale, const float* gy, float* dx, float* dtable,
+                              float* dscale, int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int k,
+                              double delta_g, void* workspace, int64_t workspace_bytes, void* stream,
+                              int64_t max_rows_hint) {
   if (k < 0 || k > UKAN_MAX_DEGREE) return UKAN_E_DEGREE;
   if (!(delta_g > 0)) return UKAN_E_GRID;
   if (!x || !base_row || !seg_start || !table || !scale || !gy || !dtable || !dscale || B < 0 ||
@@ -1175,7 +1175,7 @@ extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
   if (B > 0 && ukan_seg_ok(B, d_out, k) && getenv("UKAN_UKAN_BWD") == nullptr) {
     UKAN_DISPATCH_K(k, {
       int rc = seg_table_grad<K, true>(x, table, scale, gy, dtable, dscale, workspace, workspace_bytes, (int)B,
-                                       (int)d_in, (int)d_out, n_u * (k + 1), rm, st);
+                                       (int)d_in, (int)d_out, n_u * (k + 1), rm, st, max_rows_hint);
       if (rc) return rc;
       if (dx) {
         const int64_t pairs = B * d_in;
@@ -1197,4 +1197,33 @@ extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row,
   // the fp64 accumulator lives in the global workspace (feature segments are data dependent)
   UKAN_DISPATCH_K(k, return launch_bwd<K, true>(x, table, scale, nullptr, gy, dx, dtable, dscale, nullptr, (double*)workspace, (int)B, (int)d_in, (int)d_out, 1 << 30, rm, st););
   return UKAN_OK;
+}
+
+extern "C" int ukan_ukan_backward(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                                  const float* table, const float* scale, const float* gy, float* dx, float* dtable,
+                                  float* dscale, int64_t B, int64_t d_in, int64_t d_out, int64_t n_u, int k,
+                                  double delta_g, void* workspace, int64_t workspace_bytes, void* stream) {
+  return ukan_backward_impl(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, B, d_in, d_out, n_u, k,
+                            delta_g, workspace, workspace_bytes, stream, 0);
+}
+
+// With the key build's max_rows: dense layers (<= 67 rows per feature) on the tensor-core path, the
+// others on the sorted-merge path with max_rows bounding the per-feature row histogram (cfg4 at
+// B = 65536: ~316 rows per feature instead of the 2*B*K bound -> the per-feature sorted sweep).
+extern "C" int64_t ukan_ukan_backward2_workspace_size(int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
+                                                     int64_t max_rows, int k) {
+  const int64_t dense = ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, n_u, max_rows, k);
+  return dense > 0 ? dense : ukan_ukan_backward_workspace_size(B, d_in, d_out, n_u, k);
+}
+
+extern "C" int ukan_ukan_backward2(const float* x, const int32_t* base_row, const int32_t* seg_start,
+                                   const float* table, const float* scale, const float* gy, float* dx, float* dtable,
+                                   float* dscale, int64_t B, int64_t d_in, int64_t d_out, int64_t n_u,
+                                   int64_t max_rows, int k, double delta_g, void* workspace, int64_t workspace_bytes,
+                                   void* stream) {
+  if (ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, n_u, max_rows, k) > 0)
+    return ukan_ukan_backward_dense(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, B, d_in, d_out, n_u,
+                                    max_rows, k, delta_g, workspace, workspace_bytes, stream);
+  return ukan_backward_impl(x, base_row, seg_start, table, scale, gy, dx, dtable, dscale, B, d_in, d_out, n_u, k,
+                            delta_g, workspace, workspace_bytes, stream, max_rows);
 }

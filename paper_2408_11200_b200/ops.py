@@ -344,12 +344,12 @@ def ukan_backward_into(x, base_row, seg_start, table, scale, gy, dx, dtable, dsc
     d_out = scale.shape[1]
     n_u = table.shape[0]
     st = stream_ptr()
-    nbytes = lib.ukan_ukan_backward_dense_workspace_size(B, d_in, d_out, n_u, max_rows, k) if max_rows > 0 else 0
-    if nbytes > 0:
-        ws = torch.empty(nbytes, device=x.device, dtype=torch.uint8)
-        check(lib.ukan_ukan_backward_dense(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(gy),
-                                           ptr(dx), ptr(dtable), ptr(dscale), B, d_in, d_out, n_u, max_rows, k, delta_g,
-                                           ptr(ws), nbytes, st), "ukan_backward_dense")
+    if max_rows > 0:  # dense layers on the tensor-core path; max_rows also bounds the sorted sweep's histogram
+        nbytes = lib.ukan_ukan_backward2_workspace_size(B, d_in, d_out, n_u, max_rows, k)
+        ws = torch.empty(max(nbytes, 8), device=x.device, dtype=torch.uint8)
+        check(lib.ukan_ukan_backward2(ptr(x), ptr(base_row), ptr(seg_start), ptr(table), ptr(scale), ptr(gy), ptr(dx),
+                                      ptr(dtable), ptr(dscale), B, d_in, d_out, n_u, max_rows, k, delta_g, ptr(ws),
+                                      nbytes, st), "ukan_backward2")
         return
     nbytes = lib.ukan_ukan_backward_workspace_size(B, d_in, d_out, n_u, k)
     ws = torch.empty(max(nbytes, 8), device=x.device, dtype=torch.uint8)

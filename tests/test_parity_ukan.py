@@ -223,3 +223,13 @@ def test_ukan_dense_stack_training_step():
             g = grad[off:off + v.numel()].reshape(v.shape)
             off += v.numel()
             assert_close(g, want[li][n], what=f"layer{li}.{n}")
+
+
+def test_ukan_large_batch_sorted_sweep_with_row_hint():
+    """B = 8192 > 6144: the 2*B*K bound used to keep the batch off the per-feature sorted sweep;
+    with the key build's max_rows (ukan_ukan_backward2) it takes that sweep.  Sparse segments
+    (> 67 rows, not the dense path), a d_out that is not a multiple of 8."""
+    layer, x, gup = random_case(8192, 4, 40, 3, 0.5, 8, 8, seed=77, sigma=30.0)
+    keys = ops.ukan_build_keys(_t(x), 3, 0.5)
+    assert 67 < keys.max_rows < 2 * 8192 * 4
+    check_against_oracle(layer, x, gup)
