@@ -451,7 +451,14 @@ spline_dx64_kernel(const float* __restrict__ x, const float* __restrict__ T, con
   const int lane = threadIdx.x % 32;
   const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (pair >= (int64_t)B * d_in) return;
-  const int i = (int)(pair / B), b = (int)(pair % B);  // feature-major (see spline_dx_kernel)
+  // feature-major inside blocks of 4096 samples: the block's fp64 g rows (32 MB at d_out = 1024)
+  // stay in L2 while every feature passes over them, instead of all B rows being re-read from DRAM
+  // once per feature (cfg4 at B = 65536: 537 GB of g reads per call)
+  constexpr int kBlk = 4096;
+  const int64_t blk = (int64_t)kBlk * d_in;
+  const int64_t sb = pair / blk, rem = pair % blk;
+  const int nb = (int)min((int64_t)kBlk, (int64_t)B - sb * kBlk);
+  const int i = (int)(rem / nb), b = (int)(sb * kBlk + rem % nb);
   const float xv = x[(size_t)b * d_in + i];
   int row;
   double u;
