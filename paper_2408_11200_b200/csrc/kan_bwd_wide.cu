@@ -982,6 +982,152 @@ seg_fsweep_kernel(const int* __restrict__ row_start, const int* __restrict__ sor
     }
 }
 
+// dx from the per-feature sorted order (UKAN, K = 4; round 2).  seg_fsort left each feature's samples
+// sorted by window row; a warp takes a run of kSxRun consecutive positions of one feature, lanes
+// own 4 consecutive outputs of each 128-output chunk, and the four window rows of C' (fp64 =
+// scale * T) stay in registers while consecutive positions share the row — ~14 samples per row at
+// the cfg4 shape, so the per-element fp32 -> fp64 conversions of spline_dx64 (its bound) mostly
+// disappear.  Per position: Q_j = sum_o g[b,o] C'[row+j,o] accumulated per lane over the chunks in
+// order, a fixed xor-tree over the lanes, dx = inv_dg * sum_j w'_j(u) Q_j (layers.py:44-46, 84-88).
+constexpr int kSxRun = 4;
+template <bool UKAN>
+__global__ void __launch_bounds__(256)
+seg_dx_sorted_kernel(const int* __restrict__ row_start, const int* __restrict__ sorted_b,
+                     const double* __restrict__ sorted_u, const float* __restrict__ T, const double* __restrict__ s64,
+                     const double* __restrict__ g64, float* __restrict__ dx, int d_in, int d_out, int B, RowMap rm,
+                     Basis<4> bas) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.y;
+  const int p0 = (blockIdx.x * 8 + warp) * kSxRun;
+  if (p0 >= B) return;
+  int row0, nrows;
+  feature_rows<UKAN>(rm, i, row0, nrows);
+  const int* rs = row_start + row0 + i;  // [nrows + 1] starts of each row's run of sorted positions
+  const int pend = __ldg(rs + nrows);
+  int rowp[kSxRun], bp[kSxRun];
+  double up[kSxRun];
+  {
+    int lo = 0, hi = nrows;  // largest r with rs[r] <= p0
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(rs + mid) <= p0) lo = mid;
+      else hi = mid - 1;
+    }
+    int r = lo;
+#pragma unroll
+    for (int q = 0; q < kSxRun; ++q) {
+      const int p = p0 + q;
+      rowp[q] = -1;
+      bp[q] = 0;
+      up[q] = 0.0;
+      if (p < pend) {
+        while (r + 1 <= nrows && __ldg(rs + r + 1) <= p) ++r;
+        rowp[q] = r;
+        bp[q] = __ldg(sorted_b + (size_t)i * B + p);
+        up[q] = __ldg(sorted_u + (size_t)i * B + p);
+      }
+    }
+  }
+  double acc[kSxRun][4];
+#pragma unroll
+  for (int q = 0; q < kSxRun; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[q][j] = 0.0;
+  for (int oc = 0; oc < d_out; oc += 128) {
+    const int o = oc + 4 * lane;
+    if (o < d_out) {  // d_out % 4 == 0
+      const double2 sa = __ldg(reinterpret_cast<const double2*>(s64 + (size_t)i * d_out + o));
+      const double2 sb2 = __ldg(reinterpret_cast<const double2*>(s64 + (size_t)i * d_out + o) + 1);
+      int cur = -1;
+      double c[4][4];
+#pragma unroll
+      for (int q = 0; q < kSxRun; ++q) {
+        if (rowp[q] < 0) continue;
+        if (rowp[q] != cur) {  // the run moved to another row: its four window rows of C'
+          cur = rowp[q];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(T + (size_t)(row0 + cur + j) * d_out + o));
+            c[j][0] = sa.x * (double)t.x;
+            c[j][1] = sa.y * (double)t.y;
+            c[j][2] = sb2.x * (double)t.z;
+            c[j][3] = sb2.y * (double)t.w;
+          }
+        }
+        const double2 ga = __ldg(reinterpret_cast<const double2*>(g64 + (size_t)bp[q] * d_out + o));
+        const double2 gb = __ldg(reinterpret_cast<const double2*>(g64 + (size_t)bp[q] * d_out + o) + 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double a = acc[q][j];
+          a = fma(ga.x, c[j][0], a);
+          a = fma(ga.y, c[j][1], a);
+          a = fma(gb.x, c[j][2], a);
+          a = fma(gb.y, c[j][3], a);
+          acc[q][j] = a;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kSxRun; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double a = acc[q][j];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      acc[q][j] = a;
+    }
+  if (lane < kSxRun) {
+    double a[4], wp[4];
+    double u = 0.0;
+    int row = -1, b = 0;
+#pragma unroll
+    for (int q = 0; q < kSxRun; ++q)
+      if (q == lane) {
+        row = rowp[q];
+        b = bp[q];
+        u = up[q];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = acc[q][j];
+      }
+    if (row >= 0) {
+      basis_dweights<4>(bas, u, wp);
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t = fma(a[j], wp[j], t);
+      dx[(size_t)b * d_in + i] = (float)(t * rm.inv_dg);
+    }
+  }
+}
+
+bool seg_uses_sorted(int B, int64_t total_rows, int64_t max_rows_hint) {
+  static const bool cuda_cores = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == '1';
+  static const bool tiles_only = getenv("UKAN_SEG") != nullptr && getenv("UKAN_SEG")[0] == 't';
+  int64_t max_rows = std::min<int64_t>(total_rows, 2 * (int64_t)B * 4);
+  if (max_rows_hint > 0) max_rows = std::min<int64_t>(max_rows, max_rows_hint);
+  return !cuda_cores && !tiles_only && max_rows + 1 <= kFsMaxRows;
+}
+
+// dx on the sorted order seg_table_grad<4, true> just left in `ws` (same ws / shapes); s64 / g64:
+// fp64 copies of scale and g.
+int seg_dx_sorted(const float* T, const double* s64, const double* g64, float* dx, void* ws, int B, int d_in,
+                  int d_out, int64_t total_rows, const RowMap& rm, cudaStream_t st) {
+  const int nch = (B + kWdBC - 1) / kWdBC;
+  unsigned char* recs = reinterpret_cast<unsigned char*>(ws);
+  const int64_t rec = (((int64_t)d_in * nch * kWdBC * 12 + 255) / 256) * 256;
+  const int64_t tiles = (total_rows + kWdRT - 1) / kWdRT + d_in;
+  unsigned char* base = recs + rec + ((4 * ((int64_t)d_in + 1) + 255) / 256) * 256 +
+                        ((int64_t)sizeof(double) * tiles * d_out + 255) / 256 * 256;
+  const double* sorted_u = reinterpret_cast<const double*>(base);
+  const int* sorted_b = reinterpret_cast<const int*>(base + (int64_t)8 * d_in * B);
+  const int* row_start = reinterpret_cast<const int*>(base + ((int64_t)12 * d_in * B + 255) / 256 * 256);
+  dim3 grid((unsigned)((B + 8 * kSxRun - 1) / (8 * kSxRun)), (unsigned)d_in);
+  seg_dx_sorted_kernel<true><<<grid, 256, 0, st>>>(row_start, sorted_b, sorted_u, T, s64, g64, dx, d_in, d_out, B, rm,
+                                                    make_basis<4>(3));
+  UKAN_LAUNCH_CHECK();
+  return UKAN_OK;
+}
+
 // dscale[f,o] = sum over the feature's tiles (fixed order)
 __global__ void seg_reduce_kernel(const double* __restrict__ part, const int* __restrict__ tile_start,
                                   float* __restrict__ dscale, int d_in, int d_out) {

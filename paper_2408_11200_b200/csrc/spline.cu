@@ -603,6 +603,9 @@ int kan_bwd_wide_run(const float* x, const float* C, const float* scale, const f
                      float* dbw, void* workspace, int64_t ws_bytes, int B, int d_in, int d_out, int R,
                      const KanGrid& grid, const WidePlan& p, cudaStream_t st);
 int64_t seg_workspace(int64_t B, int64_t d_in, int64_t d_out, int64_t total_rows);
+bool seg_uses_sorted(int B, int64_t total_rows, int64_t max_rows_hint);
+int seg_dx_sorted(const float* T, const double* s64, const double* g64, float* dx, void* ws, int B, int d_in,
+                  int d_out, int64_t total_rows, const RowMap& rm, cudaStream_t st);
 bool seg_supported(int64_t B, int64_t d_out);
 template <int K, bool UKAN>
 int seg_table_grad(const float* x, const float* T, const float* scale, const float* gy, float* dT, float* dscale,
@@ -1193,6 +1196,12 @@ static int ukan_backward_impl(const float* x, const int32_t* base_row, const int
         UKAN_LAUNCH_CHECK();
         cvt_f64_kernel<<<(unsigned)((d_in * d_out + 255) / 256), 256, 0, st>>>(scale, s64, d_in * d_out);
         UKAN_LAUNCH_CHECK();
+        // A/B only (UKAN_DX_SORTED=1): dx on the sweep's sorted order — measured slower at the cfg4
+        // shape (7.4 vs 6.1 ms: latency-bound runs of 4 positions), kept for the record
+        static const bool sorted_on = getenv("UKAN_DX_SORTED") && getenv("UKAN_DX_SORTED")[0] == '1';
+        if (K == 4 && sorted_on && B <= 8192 && d_out % 4 == 0 &&
+            seg_uses_sorted((int)B, n_u * (k + 1), max_rows_hint))
+          return seg_dx_sorted(table, s64, g64, dx, workspace, (int)B, (int)d_in, (int)d_out, n_u * (k + 1), rm, st);
         spline_dx64_kernel<K, true><<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(x, table, s64, g64, dx, (int)B,
                                                                                  (int)d_in, (int)d_out, rm,
                                                                                  make_basis<K>(K - 1));
