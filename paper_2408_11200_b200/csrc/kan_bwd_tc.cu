@@ -979,15 +979,15 @@ int kan_bwd_tc_prep(const float* x, void* workspace, int64_t ws_bytes, int B, in
 static int tc_sweep_dispatch(const float* C, const float* scale, const float* gy, float* dC, float* dscale,
                              unsigned char* recs, double* part, int B, int d_in, int d_out, int G, const TcPlan& p,
                              cudaStream_t st) {
-  if (p.split && p.rb == 8 && p.wpf == 4) return tc2_launch<8, 8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
-  if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   CUtensorMap map;  // tc3: the driver's tensor-map encoder is required (else the tc2 sweep runs)
   const bool tc3 = tc3_enabled() && (d_out % 4) == 0 && ((uintptr_t)gy % 16) == 0 && p.split && p.wpf == 4 &&
                    ((p.rb == 16 && p.nt == 4) || (p.rb == 8 && p.nt == 8)) && tc3_tensor_map(&map, gy, B, d_out);
   if (tc3 && p.rb == 16) return tc3_launch<16, 4, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (tc3 && p.rb == 8) return tc3_launch<8, 8, 4, 4>(map, C, scale, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.wpf == 4) return tc2_launch<8, 8, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.nt == 8) return tc2_launch<8, 8, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8 && p.fpb == 8) return tc2_launch<8, 4, 8, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
+  if (p.split && p.rb == 8) return tc2_launch<8, 4, 4, 2>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 4) return tc2_launch<16, 4, 4, 4>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8 && p.fpb == 2) return tc2_launch<16, 8, 2, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
   if (p.split && p.rb == 16 && p.wpf == 8) return tc2_launch<16, 4, 4, 8>(C, scale, gy, dC, dscale, recs, part, B, d_in, d_out, G, p, st);
