@@ -1354,11 +1354,11 @@ static int dx_tc_launch(const float* C, const float* scale, const float* gy, flo
                         const int32_t* seg = nullptr) {
   const DxSmem L = dx_smem_layout(G);
   const int n_fg = (d_in + kDxF - 1) / kDxF;
-  // band 128: at the full cfg3 batch (B = 65536, 256 chunks) the wider band is fastest — dx + table
-  // gradient 1973 ms at band 8, 1951 at 32, 1943 at 128 (profiles/r02/dx_band_sweep.txt); at
-  // B = 16384 bands 8..32 measured equal time (band 8 moved the least DRAM: 45.8 GB per call);
-  // 16 warps x 12 tasks measured faster than 32 x 6 (64 registers spill)
-  static const int band_env = getenv("UKAN_DX_BAND") ? atoi(getenv("UKAN_DX_BAND")) : 128;
+  // band 32: at the full cfg3 batch (B = 65536, 256 chunks) wider bands are faster but re-read C'
+  // from DRAM more often — dx 1.128 s / 172 GB at band 8, 1.112 s / 201 GB at 16, 1.103 s / 294 GB
+  // at 32, 1.094 s / 993 GB at 128 (ncu, profiles/r02/dx_band_sweep.txt); 32 keeps most of the
+  // gain at 1.7x the traffic.  16 warps x 12 tasks measured faster than 32 x 6 (64 registers spill)
+  static const int band_env = getenv("UKAN_DX_BAND") ? atoi(getenv("UKAN_DX_BAND")) : 32;
   static const int warps_env = getenv("UKAN_DX_WARPS") ? atoi(getenv("UKAN_DX_WARPS")) : 16;
   const int band = std::max(1, std::min(band_env, nch));
   const int64_t nblk = (int64_t)nch * n_fg;
